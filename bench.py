@@ -1,0 +1,294 @@
+"""Benchmark: monodomain DoF*steps/s of config 2 (BASELINE.json configs[2]).
+
+One "step" = one IMEX-BDF2 monodomain time step (TissueSolver.step,
+reference simulation.py:425-483) of the 20x7x3 mm TTP06 slab at h=0.1 mm
+(442,401 nodes): fused ionic update + RHS + Jacobi PCG + activation.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* ours: warm-up W steps from rest, then K timed steps (the propagation phase:
+  the stimulus fires at t=0, CG needs 7..18 iterations per step).  `value` is
+  device-timed (CUDA events, barrier + synchronize both sides, max over
+  ranks) with all state resident in HBM; `e2e` goes through the public API
+  with host buffers: the initial state is uploaded from a host checkpoint
+  payload (TissueSolver.restore) inside the timed region, and every step
+  reads back the run() output row (t, u_min, u_max, 9 probes) to the host.
+* reference: the reference algorithm on the host CPU cores (oracle port,
+  oracle/, pinned bit-identical to the reference; the reference itself is
+  Python+numba and cannot travel to the GPU box) on a bounded sample of the
+  same workload.
+
+The ionic state ring (4 x 18 x 442,401 doubles = 255 MB) exceeds the 126 MB
+L2, so no explicit L2 flush is done between steps.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "monodomain DoF*steps/s (config 2: TTP06 slab 442,401 nodes, BDF2, Jacobi PCG)"
+UNIT = "DoF*steps/s"
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"],
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_sample(steps, threads=None):
+    """Oracle port of the reference step on cfg 2, `steps` steps from rest."""
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import configs
+
+    ns = configs.this_package()
+    cfg = configs.config2(ns)
+    orc = O.OracleTissue(cfg)
+    orc.step()                        # first step (builds A for alpha=1)
+    orc.step()                        # alpha=1.5 system
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        orc.step()
+    wall = time.perf_counter() - t0
+    n = cfg.mesh.nodes.shape[0]
+    return n * steps / wall, wall, O.num_threads(), orc.iters[2:]
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    value, wall, cores, its = cpu_sample(args.ref_steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.ref_steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2 TTP06 slab 20x7x3 mm h=0.1 mm, BDF2, dt=2e-5 s",
+                   "nodes": 442401},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"steps 3..{2 + args.ref_steps} of config 2 from rest "
+                                   f"(CG iterations {min(its)}..{max(its)})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    ns = configs.this_package()
+    cfg = configs.config2(ns)
+    n = cfg.mesh.nodes.shape[0]
+    solver = TissueSolver(cfg)
+    init_payload = solver.checkpoint_payload()   # host copy of the initial state
+    for _ in range(args.warmup):
+        solver.enqueue_step()
+    solver.sync()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed region ------------------------------------------------
+    ev_ionic = []
+    launches0 = solver.launches
+    barrier()
+    with ClockSampler(local) as clocks:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            solver.enqueue_step(events=(e1, e2))
+            ev_ionic.append((e0, e1, e2))
+        end.record()
+        barrier()
+    launches = solver.launches - launches0
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ionic_ms = np.array([a.elapsed_time(b) for a, b, _ in ev_ionic])
+    solve_ms = np.array([b.elapsed_time(c) for _, b, c in ev_ionic])
+    its = solver.iterations_log()[-args.steps:]
+    solver.sync()
+
+    # ---- end-to-end through the public API ----------------------------------
+    e2e_solver = TissueSolver(cfg)
+    probes = [ns.nearest_node(cfg.mesh, p) for p in configs.corner_probes()]
+    probes.append(ns.nearest_node(cfg.mesh, (10e-3, 3.5e-3, 1.5e-3)))
+    pidx = torch.tensor(probes, device="cuda")
+    pinned = torch.empty(2 + len(probes), dtype=torch.float64, pin_memory=True)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_solver.restore(init_payload)
+    for _ in range(args.warmup):
+        e2e_solver.enqueue_step()
+    for _ in range(args.steps):
+        e2e_solver.enqueue_step()
+        u = e2e_solver.potential_device
+        mm = torch.aminmax(u)
+        row = torch.cat([mm.min.reshape(1), mm.max.reshape(1), u[pidx]])
+        pinned.copy_(row, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    barrier()
+    e2e_wall = time.perf_counter() - t0
+    e2e_steps = args.steps + args.warmup
+    e2e_value = n * e2e_steps * world / e2e_wall
+
+    hbm, peak_kind = peaks()
+    order = 2
+    nv = 18
+    # algorithmic bytes of the fused TTP06 update (BDF2, single volume):
+    # read u_n,u_{n-1}, W_n,W_{n-1}; write W_{n+1}, I, combo, x0
+    ionic_bytes = n * 8 * (order + order * nv + nv + 3)
+    pcg_share = float(solve_ms.sum() / (ionic_ms.sum() + solve_ms.sum()))
+    ionic_avg = float(ionic_ms.mean()) * 1e-3
+    achieved = ionic_bytes / ionic_avg / 1e9
+    line = {
+        "metric": METRIC, "value": n * args.steps * world / (ms * 1e-3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2 TTP06 slab 20x7x3 mm h=0.1 mm (442,401 nodes), "
+                               "BDF2, dt=2e-5 s, steps from rest (propagation phase)",
+                   "operator": "stencil27 class tables" if solver.op.kind == 1 else "csr",
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "state ring 255 MB > L2; no flush",
+                   "cg_iters_per_step": [int(its.min()), float(its.mean()), int(its.max())]},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+        "kernels": {"ionic_ms": float(ionic_ms.mean()), "pcg_ms": float(solve_ms.mean()),
+                    "pcg_share": pcg_share},
+        "roofline": {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2>",
+                     "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / hbm,
+                     "bytes_per_launch": ionic_bytes, "traffic": None},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": len(init_payload) / e2e_steps,
+                "d2h_bytes_per_step": 8 * (2 + len(probes))},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        value, wall, cores, cits = cpu_sample(args.cpu_steps)
+        line["cpu_baseline"] = {
+            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle port, steps 3..{2 + args.cpu_steps} of config 2 from rest"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--ref-steps", type=int, default=12)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,240 @@
+/*
+ * mdx.h - C ABI of the B200 (sm_100a) monodomain hot path.
+ *
+ * Every data pointer is a DEVICE pointer owned by the caller; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). Calls are stream-ordered and
+ * asynchronous; none allocates device memory or synchronises. Return value:
+ * MDX_OK (0) or a negative MDX_ERR_* code with text in mdx_last_error().
+ * Numerical failures detected on the device (CG divergence, non-finite
+ * solution) are reported through the caller's `status` word, never by
+ * return code, so launches stay asynchronous.
+ *
+ * The reference (lifex-ep re-implementation, /root/reference/pkg) is
+ * Python + numba; each entry point below names the reference function it
+ * replaces. The Python package paper_2308_01651_b200 binds this header with
+ * ctypes (see INTEGRATION.md for the binding a reference maintainer adds).
+ */
+#ifndef MDX_H
+#define MDX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDX_ABI_VERSION 1
+
+#define MDX_OK 0
+#define MDX_ERR_ARG (-1)
+#define MDX_ERR_CUDA (-2)
+#define MDX_ERR_SIZE (-3)
+
+/* ionic/__init__.py:40-49 model_module(kind) */
+#define MDX_MODEL_ALIEV_PANFILOV 0
+#define MDX_MODEL_BUENO_OROVIO 1
+#define MDX_MODEL_TTP06 2
+
+#define MDX_OP_STENCIL27 1 /* structured hex slab, node-class tables */
+#define MDX_OP_CSR 2       /* assembled CSR, int64 indptr / int32 indices */
+
+#define MDX_MAX_LIFT 8 /* volumes in the ICI lift (simulation.py:342-352) */
+
+const char* mdx_last_error(void);
+int mdx_abi_version(void);
+
+/* --------------------------------------------------------------------- */
+/* Ionic-model module protocol (ionic/__init__.py:1-11)                   */
+/* State element (i, v) lives at W[i*cs + v*vs]: AoS (cs=nv, vs=1) as the */
+/* reference's (N, nv) arrays, or SoA (cs=1, vs=ld).                      */
+/* --------------------------------------------------------------------- */
+int mdx_ionic_num_vars(int model);   /* <model>.NUM_VARS */
+int mdx_ionic_num_params(int model); /* len(<model>.pack(...)) */
+
+/* <model>.advance_kernel(u_ext, W_ext, W_bdf, alpha, dt, P, W_out, I_out)
+ *   bueno_orovio.py:152-186, ten_tusscher.py:374-403, aliev_panfilov.py:82-95.
+ * P is a HOST array of np doubles (it is passed by value to the kernel).
+ * clamp_count (device, may be NULL) accumulates the returned clamp count. */
+int mdx_ionic_advance(int model, int64_t n, const double* u_ext, const double* W_ext,
+                      const double* W_bdf, int64_t cs, int64_t vs, double alpha, double dt,
+                      const double* P, int np, double* W_out, double* I_out,
+                      unsigned long long* clamp_count, void* stream);
+
+/* <model>.current_kernel(u, W, P, I_out)
+ *   bueno_orovio.py:146-149, ten_tusscher.py:368-371, aliev_panfilov.py:75-79 */
+int mdx_ionic_current(int model, int64_t n, const double* u, const double* W, int64_t cs,
+                      int64_t vs, const double* P, int np, double* I_out, void* stream);
+
+/* <model>.point_rates(u, w, P) -> (I, dw) for n points, AoS W and dW
+ *   bueno_orovio.py:135-143, ten_tusscher.py:353-365, aliev_panfilov.py:62-72 */
+int mdx_ionic_point_rates(int model, int64_t n, const double* u, const double* W,
+                          const double* P, int np, double* I_out, double* dW, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* Tissue step, part 1: ionic update of one volume                        */
+/*   TissueSolver.step ionic section, simulation.py:440-455, plus the      */
+/*   HistoryRing.weighted_sum combinations it consumes (timestepping.py:89) */
+/* Rings: slot s of the potential at u_ring + s*ldu; slot s of a volume's  */
+/* state, variable v, at w_ring + (s*nv + v)*ldw. `head` is the slot of    */
+/* the newest entry; the update writes slot (head+1) % ring_slots.         */
+/* --------------------------------------------------------------------- */
+typedef struct mdx_tissue_ionic_args {
+  int64_t n;             /* DOFs of this volume (or all nodes for prep) */
+  const int32_t* dofs;   /* volume DOF -> node id; NULL = identity */
+  double* u_ring;        /* potential ring */
+  int64_t ldu;
+  double* w_ring;        /* ionic state ring of this volume (SoA) */
+  int64_t ldw;
+  int32_t ring_slots;    /* >= order + 1 */
+  int32_t head;
+  int32_t order;         /* BDF order of this step, min(step+1, bdf_order) */
+  int32_t prep;          /* 1: also write combo and x0 (identity map only) */
+  double dt;
+  double* i_out;         /* full-length current of this volume (by node id) */
+  unsigned long long* clamp_count; /* may be NULL */
+  /* prep outputs: combo = u_BDF/dt + I_app (simulation.py:457-461) and the
+   * CG warm start x0 = u_EXT written into the u ring's next slot */
+  double* combo;
+  const double* profiles; /* [n_impulses][ldp] applied-current profiles / C_m */
+  int64_t ldp;
+  uint64_t active_mask;  /* impulses whose window is open at t_{n+1} */
+  int32_t n_impulses;
+  int32_t _pad;
+  const int32_t* status; /* nonzero => an earlier step failed: no-op */
+} mdx_tissue_ionic_args;
+
+int mdx_tissue_ionic(int model, const mdx_tissue_ionic_args* args, const double* P, int np,
+                     void* stream);
+/* combo/x0 pass over all nodes when several volumes share the mesh */
+int mdx_tissue_prep(const mdx_tissue_ionic_args* args, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* Tissue step, part 2 / linear solver: persistent Jacobi PCG             */
+/*   JacobiCg.solve + _cg_kernel (linalg.py:34-105); in tissue mode also   */
+/*   the RHS assembly (simulation.py:457-465, fem.py:489-504), the         */
+/*   finiteness check (:473-476) and _update_activation (:485-494).        */
+/* --------------------------------------------------------------------- */
+typedef struct mdx_operator {
+  int32_t kind;          /* MDX_OP_STENCIL27 or MDX_OP_CSR */
+  int32_t ncls;          /* stencil: number of node classes */
+  int64_t n;             /* rows = nodes */
+  int32_t nx1, ny1, nz1; /* stencil: nodes per axis (x fastest) */
+  int32_t _pad;
+  const uint16_t* cls;   /* stencil: class id of every node */
+  const int64_t* indptr; /* csr */
+  const int32_t* indices;
+  int64_t nnz;
+} mdx_operator;
+
+typedef struct mdx_cg_args {
+  mdx_operator op;
+  /* operator values: stencil -> [ncls][27] class tables; csr -> [nnz] */
+  const double* a_val;   /* (alpha/dt) M + K, inactive rows = identity */
+  const double* dinv;    /* 1/diag(A): stencil [ncls], csr [n] */
+  /* right-hand side: plain solve */
+  const double* b;
+  /* right-hand side: tissue (b == NULL) */
+  const double* m_val;   /* M */
+  const double* combo;   /* u_BDF/dt + I_app */
+  int32_t n_lift;        /* ICI lift terms sum_v M^v I^v */
+  int32_t step;          /* step index recorded on failure */
+  const double* lift_val[MDX_MAX_LIFT];
+  const double* lift_cur[MDX_MAX_LIFT];
+  const uint8_t* inactive; /* stencil: per class; csr: per node; NULL = none */
+  const double* rest;      /* pinned value of inactive rows */
+  const double* thr;       /* activation threshold */
+  /* vectors */
+  double* x;             /* in: warm start (u_EXT); out: solution */
+  double* p;             /* work, n doubles */
+  /* activation map (tissue; act_time NULL = skip) */
+  const double* u_prev;
+  double* act_time;
+  double* best_slope;
+  uint8_t* frozen;
+  double t_next, dt;
+  double tol;
+  int32_t max_iter;
+  int32_t partials_capacity; /* blocks the partials buffer can hold */
+  double* partials;      /* [partials_capacity][4] */
+  unsigned int* barrier; /* [2], zero-initialised once, reused */
+  int32_t* iters_out;    /* iterations (reference convention: -max_iter) */
+  double* relres_out;
+  int32_t* status;       /* nonzero on entry => no-op; bit0 diverged, bit1 non-finite */
+  int32_t* fail_step;    /* receives `step` when status is raised */
+} mdx_cg_args;
+
+/* npt_hint: minimum nodes per thread (0 = automatic) */
+int mdx_pcg_solve(const mdx_cg_args* args, int tissue, int npt_hint, void* stream);
+/* y = A x with the same row arithmetic (csr_matvec, linalg.py:17-23) */
+int mdx_spmv(const mdx_cg_args* args, const double* x, double* y, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* Setup: operator assembly (fem.py:280-426, bit-identical)               */
+/* --------------------------------------------------------------------- */
+typedef struct mdx_assembly_args {
+  int64_t n_elem;
+  int32_t nl;            /* 8 hex, 4 tet */
+  int32_t nq;
+  const double* nodes;   /* [n][3] */
+  const int32_t* elements; /* [n_elem][nl] */
+  const double* quad_w;    /* HOST [nq] */
+  const double* quad_basis;/* HOST [nq][nl] */
+  const double* quad_grad; /* HOST [nq][nl][3] */
+  const int32_t* sigma_row;/* [n_elem], -1 = no conduction; NULL = mass only */
+  const double* sigmas;    /* [rows][3] (sigma_l, sigma_t, sigma_n) */
+  const double* f0;        /* [n][3] */
+  const double* s0;        /* [n][3] */
+  double* K_local;         /* [n_elem][nl][nl] or NULL */
+  double* M_local;         /* [n_elem][nl][nl] or NULL */
+} mdx_assembly_args;
+
+int mdx_assemble_local(const mdx_assembly_args* args, void* stream);
+int mdx_scatter_csr(int64_t n, int nl, const int32_t* elements, const int64_t* inc_ptr,
+                    const int32_t* inc_elem, const int8_t* inc_local, const uint8_t* include,
+                    const double* local, const int64_t* indptr, const int32_t* indices,
+                    double* data, void* stream);
+int mdx_stencil_rows(int nx, int ny, int nz, const uint8_t* include, const double* local,
+                     double* rows, void* stream);
+int mdx_hash_rows(int64_t n, int width, const double* rows, unsigned long long* out,
+                  void* stream);
+int mdx_verify_classes(int64_t n, int width, const double* rows, const uint16_t* cls,
+                       const int64_t* rep, unsigned long long* mismatches, void* stream);
+/* A = c*M + K entrywise (simulation.py:398) */
+int mdx_combine_system(int64_t m, double c, const double* M, const double* K, double* A,
+                       void* stream);
+
+/* --------------------------------------------------------------------- */
+/* 0D pacing batch: pace_single_cell (ionic/__init__.py:119-167) for many  */
+/* cells at once, state and BDF history register-resident (config 1).     */
+/* --------------------------------------------------------------------- */
+typedef struct mdx_pace_args {
+  int64_t n_cells;
+  double* u;             /* [n_cells] in: initial, out: final */
+  double* W;             /* [nv][ldw] SoA, in/out */
+  int64_t ldw;
+  double* peak;          /* [n_cells] running max of u, or NULL */
+  int32_t order;         /* target BDF order (ramped from 1) */
+  int32_t n_pulses;
+  int64_t n_steps;
+  double dt;
+  int64_t n_stim_cells;  /* cells [0, n_stim_cells) receive the protocol */
+  double period;
+  double pulse_t0[8];
+  double pulse_dur[8];
+  double pulse_amp[8];
+  int64_t n_trace_cells; /* cells [0, n_trace_cells) record a trace */
+  int64_t trace_rows;
+  int64_t stride;
+  double* trace;         /* [n_trace_cells][trace_rows][2+nv] */
+  unsigned long long* clamp_count;
+  int32_t* status;       /* bit0: a cell lost finiteness */
+} mdx_pace_args;
+
+int mdx_pace_cells(int model, const mdx_pace_args* args, const double* P, int np,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MDX_H */

@@ -1,0 +1,173 @@
+"""Device-resident tissue operators: class-table stencil and CSR.
+
+The tissue step needs, per node row i: the system matrix A = (alpha/dt) M + K
+for each BDF phase, the mass M for the RHS, the per-volume masses M^v of the
+ICI lift, the inactive flag with its pinned resting value, the activation
+threshold, and 1/A_ii (`/root/reference/pkg/src/monodomain/simulation.py:
+327-413`).
+
+`StencilOperator` (structured hex slabs): every node row has at most 27
+entries at fixed lattice offsets, and rows repeat: a uniform slab has 27
+distinct row patterns (interior, faces, edges, corners); a slab with a scar
+has a few hundred.  The device computes every node's row bits from the
+element matrices, hashes them, and the host groups equal rows into classes.
+A node then costs 2 bytes (its class id) and the operator streams no matrix
+data at all - the "matrix-free" apply with exactly the reference's entries.
+
+`CsrOperator` (any mesh): the reference pattern with device-assembled values.
+"""
+
+import numpy as np
+
+from . import _native as N
+from .timestepping import ALPHA
+
+STENCIL_CENTER = 13
+MAX_CLASSES = 65535
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _combine_host(c, M, K):
+    """c*M + K with two roundings (numpy never fuses), scipy's arithmetic."""
+    return c * M + K
+
+
+class StencilOperator:
+    kind = N.OP_STENCIL27
+
+    def __init__(self, dm, lattice, K_local, M_local, include_k, include_m,
+                 lift_includes, inactive, rest, thr, dt, orders):
+        torch = _torch()
+        nx, ny, nz = lattice
+        self.lattice = lattice
+        self.n = dm.n
+        rows_k = dm.stencil_rows(lattice, K_local, include_k)
+        rows_m = dm.stencil_rows(lattice, M_local, include_m)
+        lift_rows = [rows_m if inc is None else dm.stencil_rows(lattice, M_local, inc)
+                     for inc in lift_includes]
+        extra = torch.from_numpy(np.column_stack([
+            inactive.astype(np.float64), rest.astype(np.float64),
+            thr.astype(np.float64)])).cuda()
+        key = torch.cat([rows_k, rows_m, *lift_rows, extra], dim=1).contiguous()
+        width = key.shape[1]
+        hashes = torch.empty(self.n, dtype=torch.int64, device="cuda")
+        N.check(N.lib().mdx_hash_rows(self.n, width, N.ptr(key), N.ptr(hashes),
+                                      N.stream_handle()), "mdx_hash_rows")
+        h = hashes.cpu().numpy()
+        uniq, first, inverse = np.unique(h, return_index=True, return_inverse=True)
+        if uniq.size > MAX_CLASSES:
+            raise OverflowError(f"{uniq.size} stencil classes exceed {MAX_CLASSES}")
+        self.ncls = int(uniq.size)
+        self.cls = torch.from_numpy(inverse.astype(np.uint16)).cuda()
+        rep = torch.from_numpy(first.astype(np.int64)).cuda()
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        N.check(N.lib().mdx_verify_classes(self.n, width, N.ptr(key), N.ptr(self.cls),
+                                           N.ptr(rep), N.ptr(bad), N.stream_handle()),
+                "mdx_verify_classes")
+        if int(bad.item()):
+            raise OverflowError("stencil row hash collision")
+        tab = key[rep].cpu().numpy()
+        nl = len(lift_rows)
+        self.tab_k = np.ascontiguousarray(tab[:, 0:27])
+        self.tab_m = np.ascontiguousarray(tab[:, 27:54])
+        self.tab_lift = [np.ascontiguousarray(tab[:, 54 + 27 * v: 81 + 27 * v])
+                         for v in range(nl)]
+        base = 54 + 27 * nl
+        self.cls_inactive = tab[:, base] != 0.0
+        self.cls_rest = np.ascontiguousarray(tab[:, base + 1])
+        self.cls_thr = np.ascontiguousarray(tab[:, base + 2])
+        del key, rows_k, rows_m, lift_rows
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+        self.d_m = up(self.tab_m.ravel())
+        self.d_lift = [self.d_m if inc is None else up(t.ravel())
+                       for inc, t in zip(lift_includes, self.tab_lift)]
+        self.d_inactive = up(self.cls_inactive.astype(np.uint8))
+        self.d_rest = up(self.cls_rest)
+        self.d_thr = up(self.cls_thr)
+        self.a_tables, self.dinv = {}, {}
+        self.host_a = {}
+        for order in orders:
+            c = ALPHA[order] / dt
+            A = _combine_host(c, self.tab_m, self.tab_k)
+            diag = A[:, STENCIL_CENTER].copy()
+            diag[self.cls_inactive] = 1.0
+            A[:, STENCIL_CENTER] = diag
+            if (diag <= 0).any():
+                raise ValueError("system matrix has non-positive diagonal")
+            self.host_a[order] = A
+            self.a_tables[order] = up(A.ravel())
+            self.dinv[order] = up(1.0 / diag)
+
+    def operator(self):
+        op = N.Operator()
+        op.kind = N.OP_STENCIL27
+        op.ncls = self.ncls
+        op.n = self.n
+        op.nx1, op.ny1, op.nz1 = (d + 1 for d in self.lattice)
+        op.cls = N.ptr(self.cls)
+        return op
+
+    def device_bytes(self):
+        return 2 * self.n
+
+
+class CsrOperator:
+    kind = N.OP_CSR
+
+    def __init__(self, dm, space, K_local, M_local, include_k, include_m,
+                 lift_includes, inactive, rest, thr, dt, orders):
+        torch = _torch()
+        indptr, indices = space.pattern()
+        self.n = dm.n
+        self.nnz = int(indices.size)
+        self.indptr = torch.from_numpy(indptr).cuda()
+        self.indices = torch.from_numpy(indices).cuda()
+        vk = dm.csr_values(space, K_local, include_k)
+        self.d_m = dm.csr_values(space, M_local, include_m)
+        self.d_lift = [self.d_m if inc is None else dm.csr_values(space, M_local, inc)
+                       for inc in lift_includes]
+        diag_pos = np.full(self.n, -1, dtype=np.int64)
+        rows = np.repeat(np.arange(self.n), np.diff(indptr))
+        on_diag = np.flatnonzero(rows == indices)
+        diag_pos[rows[on_diag]] = on_diag
+        if (diag_pos < 0).any():
+            raise ValueError("system matrix has non-positive diagonal")
+        dpos = torch.from_numpy(diag_pos).cuda()
+        inact = torch.from_numpy(inactive.astype(np.bool_)).cuda()
+        self.d_inactive = torch.from_numpy(inactive.astype(np.uint8)).cuda()
+        self.d_rest = torch.from_numpy(np.ascontiguousarray(rest, np.float64)).cuda()
+        self.d_thr = torch.from_numpy(np.ascontiguousarray(thr, np.float64)).cuda()
+        self.a_tables, self.dinv = {}, {}
+        for order in orders:
+            c = ALPHA[order] / dt
+            A = torch.empty(self.nnz, dtype=torch.float64, device="cuda")
+            N.check(N.lib().mdx_combine_system(self.nnz, c, N.ptr(self.d_m), N.ptr(vk),
+                                               N.ptr(A), N.stream_handle()),
+                    "mdx_combine_system")
+            diag = A[dpos]
+            diag = torch.where(inact, torch.ones_like(diag), diag)
+            A[dpos] = diag
+            if bool((diag <= 0).any()):
+                raise ValueError("system matrix has non-positive diagonal")
+            self.a_tables[order] = A
+            self.dinv[order] = 1.0 / diag
+
+    def operator(self):
+        op = N.Operator()
+        op.kind = N.OP_CSR
+        op.n = self.n
+        op.indptr = N.ptr(self.indptr)
+        op.indices = N.ptr(self.indices)
+        op.nnz = self.nnz
+        return op
+
+    def device_bytes(self):
+        return 12 * self.nnz + 8 * (self.n + 1)

@@ -1,0 +1,864 @@
+"""The coupled monodomain time loop, device-resident.
+
+Drop-in mirror of `/root/reference/pkg/src/monodomain/simulation.py`:
+stimulus types (`:48-115`), configuration dataclasses (`:123-218`),
+`SectionTimer` (`:225-254`), `TissueSolver` (`:293-604`), checkpoints
+(`:518-631`) and `run` (`:651-716`).  `TissueSolver` accepts these
+configuration objects or the reference's own (duck-typed), so one config
+drives both solvers.
+
+Per step the device runs, with no host round trip:
+
+1. `mdx_tissue_ionic` per volume: BDF combinations of the potential and
+   ionic-state rings, closed-form gate update, explicit non-gates, I_ion at
+   the new state; for a single volume also the RHS nodal term
+   `combo = u_BDF/dt + I_app` and the warm start `x0 = u_EXT`
+   (`mdx_tissue_prep` does that pass when several volumes share the mesh);
+2. `mdx_pcg_solve` (tissue mode): one cooperative launch assembling
+   `b = M combo - sum_v M^v I^v` (inactive rows pinned), running Jacobi PCG
+   to `||r|| <= tol ||b||`, checking finiteness and updating the
+   activation map.
+
+The host only enqueues launches; per-step scalars (BDF order, t_{n+1},
+which stimulus windows are open) are computed on the host exactly as the
+reference computes them (accumulated time, left-closed windows) and passed
+as kernel arguments.  Device failures set a status word that makes every
+later launch a no-op; the host notices at its next synchronisation point,
+rolls its step counter back to the failed step and raises the reference's
+exception (`SolverDivergence`, `NonFiniteSolution`).
+"""
+
+import struct
+import time
+import zlib
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _native as N
+from .errors import (ConfigError, CorruptFile, DofCountMismatch, NonFiniteSolution,
+                     NonFiniteState, SolverDivergence, VersionMismatch)
+from .fem import ConductivitySet, DeviceMesh, FeSpace, _sigma_table, detect_lattice
+from .geometry import ElementKind, nearest_node
+from .ionic import IonicModelSpec, ModelKind, CellType, pace_single_cell
+from .ionic import model_module
+from .operators import CsrOperator, StencilOperator
+from .outputs import OutputConfig, write_csv, write_vtk
+from .timestepping import ALPHA, bdf_coefficients
+
+ACTIVATION_SENTINEL = -1.0
+RING_SLOTS = 4
+
+
+# ---------------------------------------------------------------------------
+# Stimuli (simulation.py:48-115)
+# ---------------------------------------------------------------------------
+
+
+class StimulusShape(Enum):
+    CUBIC = "Cubic"
+    SPHERICAL = "Spherical"
+    GAUSSIAN = "Gaussian"
+
+
+@dataclass
+class StimulusProtocol:
+    shape: StimulusShape
+    sites: tuple
+    amplitudes: tuple
+    extents: tuple
+    initial_times: tuple
+    durations: tuple
+    period: float = 0.0
+
+    def __post_init__(self):
+        lists = (self.sites, self.amplitudes, self.extents, self.initial_times,
+                 self.durations)
+        if len({len(x) for x in lists}) != 1:
+            raise ValueError("stimulus lists must all have the same length")
+        if any(d <= 0 for d in self.durations):
+            raise ValueError("stimulus durations must be positive")
+        if self.period != 0 and self.durations and self.period <= max(self.durations):
+            raise ValueError("stimulus period must exceed every duration")
+
+    def window_active(self, index, t):
+        s = t - self.initial_times[index]
+        if s < 0.0:
+            return False
+        if self.period > 0.0:
+            s -= self.period * np.floor(s / self.period)
+        return s < self.durations[index]
+
+    def spatial_factor(self, coords, index):
+        site = np.asarray(self.sites[index], dtype=np.float64)
+        amp = self.amplitudes[index]
+        extent = self.extents[index]
+        shape = StimulusShape(self.shape.value)
+        if shape is StimulusShape.CUBIC:
+            half = extent / 2.0
+            inside = (np.abs(coords - site) <= half * (1 + 1e-12)).all(axis=1)
+            return amp * inside.astype(np.float64)
+        d2 = ((coords - site) ** 2).sum(axis=1)
+        if shape is StimulusShape.SPHERICAL:
+            return amp * (d2 <= extent * extent * (1 + 1e-12)).astype(np.float64)
+        return amp * np.exp(-d2 / (2.0 * extent * extent))
+
+
+def applied_current(protocols, x, t):
+    point = np.asarray(x, dtype=np.float64).reshape(1, 3)
+    total = 0.0
+    for protocol in protocols:
+        for i in range(len(protocol.sites)):
+            if protocol.window_active(i, t):
+                total += protocol.spatial_factor(point, i)[0]
+    return float(total)
+
+
+# ---------------------------------------------------------------------------
+# Configuration (simulation.py:123-218)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class VolumeConfig:
+    label: str
+    material_ids: tuple
+    ionic: object
+    sigma_l: float = 0.0
+    sigma_t: float = 0.0
+    sigma_n: float = 0.0
+    disabled: bool = False
+    prepacing_time: float = 0.0
+    prepacing_protocol: object = None
+    zero_d_csv_path: str = None
+
+    def __post_init__(self):
+        self.material_ids = tuple(int(m) for m in self.material_ids)
+        if not self.material_ids:
+            raise ValueError(f"volume {self.label!r} claims no material IDs")
+
+
+@dataclass
+class LinearSolverConfig:
+    tolerance: float = 1e-10
+    max_iterations: int = 2000
+
+
+@dataclass
+class ActivationConfig:
+    enabled: bool = False
+    path: str = "activation.vtk"
+    threshold: float = None
+
+
+@dataclass
+class CheckpointConfig:
+    enabled: bool = False
+    path: str = "checkpoint.bin"
+
+
+@dataclass
+class SimulationConfig:
+    mesh: object
+    fibers: object
+    volumes: tuple
+    bdf_order: int = 2
+    dt: float = 1e-4
+    final_time: float = 1e-3
+    degree: int = 1
+    stimuli: tuple = ()
+    membrane_capacitance: float = 1.0
+    chi_m: float = 1.0
+    linear_solver: LinearSolverConfig = field(default_factory=LinearSolverConfig)
+    output: OutputConfig = field(default_factory=OutputConfig)
+    activation: ActivationConfig = field(default_factory=ActivationConfig)
+    checkpoint: CheckpointConfig = field(default_factory=CheckpointConfig)
+
+    def validate(self):
+        return validate_config(self)
+
+
+def validate_config(config):
+    """SimulationConfig.validate (simulation.py:190-218), duck-typed."""
+    if config.dt <= 0:
+        raise ConfigError("Time solver/Time step", "must be positive")
+    if config.final_time <= 0:
+        raise ConfigError("Time solver/Final time", "must be positive")
+    if config.membrane_capacitance <= 0 or config.chi_m <= 0:
+        raise ConfigError("Dimensional rescaling", "factors must be positive")
+    bdf_coefficients(config.bdf_order)
+    claimed = {}
+    for vol in config.volumes:
+        for mat in vol.material_ids:
+            if mat in claimed:
+                raise ConfigError(f"{vol.label}/Material IDs",
+                                  f"material {mat} already claimed by {claimed[mat]!r}")
+            claimed[mat] = vol.label
+    present = {int(m) for m in np.unique(config.mesh.material_ids)}
+    unclaimed = present - set(claimed)
+    if unclaimed:
+        raise ConfigError("Physical constants and models",
+                          f"mesh materials {sorted(unclaimed)} not claimed by any volume")
+    return config
+
+
+# ---------------------------------------------------------------------------
+# Timing (simulation.py:225-254): same five sections; device sections are
+# timed with CUDA events when `timed=True` (otherwise host enqueue time).
+# ---------------------------------------------------------------------------
+
+TIMING_SECTIONS = ("Initialization", "Ionic model update", "Monodomain assembly",
+                   "Linear solver", "Other")
+
+
+class SectionTimer:
+    def __init__(self):
+        self._host = {name: 0.0 for name in TIMING_SECTIONS}
+        self._events = []
+
+    class _Span:
+        def __init__(self, timer, name):
+            self.timer, self.name = timer, name
+
+        def __enter__(self):
+            self.start = time.perf_counter()
+            return self
+
+        def __exit__(self, *exc):
+            self.timer._host[self.name] += time.perf_counter() - self.start
+            return False
+
+    def section(self, name):
+        return self._Span(self, name)
+
+    def device_span(self, name, start, end):
+        self._events.append((name, start, end))
+
+    @property
+    def totals(self):
+        out = dict(self._host)
+        if self._events:
+            self._events[-1][2].synchronize()
+            for name, s, e in self._events:
+                out[name] += s.elapsed_time(e) * 1e-3
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Duck-typed views of (possibly reference-built) config objects
+# ---------------------------------------------------------------------------
+
+
+def _spec_of(ionic):
+    """IonicModelSpec of this package from any spec-like object."""
+    if isinstance(ionic, IonicModelSpec):
+        return ionic
+    kind = ModelKind.from_name(ionic.kind.value)
+    ct = None if ionic.cell_type is None else CellType.from_name(ionic.cell_type.value)
+    mod = model_module(kind)
+    defaults = mod.default_parameters()
+    overrides = {k: v for k, v in ionic.parameters.items() if defaults.get(k) != v}
+    from .ionic.base import CellState
+
+    st = ionic.initial_state
+    return IonicModelSpec(kind, ct, overrides, CellState(float(st.u), np.array(st.w)))
+
+
+class _Volume:
+    def __init__(self, config, space, threshold_override):
+        self.config = config
+        self.spec = _spec_of(config.ionic)
+        self.module = model_module(self.spec.kind)
+        if self.module.MODEL_ID is None and not config.disabled:
+            raise NotImplementedError(f"{self.spec.kind.value} has no kernels")
+        self.packed = self.module.pack(self.spec.parameters, self.spec.cell_type)
+        self.dofs = np.unique(np.concatenate(
+            [space.dofs_in_subdomain(m) for m in config.material_ids]))
+        self.num_vars = self.module.NUM_VARS
+        self.rest_u = float(self.spec.initial_state.u)
+        self.threshold = (threshold_override if threshold_override is not None
+                          else self.module.ACTIVATION_THRESHOLD)
+        self.w_ring = None
+        self.w_fill = 1
+
+    def initial_cell_state(self, order):
+        cfg = self.config
+        if cfg.disabled or cfg.prepacing_time <= 0.0:
+            return self.spec.initial_state, None
+        return pace_single_cell(self.spec, cfg.prepacing_protocol, order=order)
+
+
+def _pad(n):
+    return (n + 31) // 32 * 32
+
+
+class TissueSolver:
+    """Owns the device operators and state; advances the coupled system."""
+
+    def __init__(self, config, operator="auto", npt_hint=0, timed=False):
+        validate_config(config)
+        self.config = config
+        self.timer = SectionTimer()
+        self.timed = timed
+        self.npt_hint = npt_hint
+        with self.timer.section("Initialization"):
+            self._initialize(operator)
+
+    # -- setup ---------------------------------------------------------------
+
+    def _initialize(self, operator):
+        import torch
+
+        N.lib()
+        cfg = self.config
+        mesh = cfg.mesh
+        self.space = FeSpace(mesh, cfg.degree)
+        n = self.space.num_dofs
+        self.n = n
+        self.dt = cfg.dt
+        self.step_index = 0
+        self.time = 0.0
+        self.volumes = [_Volume(v, self.space, cfg.activation.threshold)
+                        for v in cfg.volumes]
+        by_desc = sorted(self.volumes, key=lambda v: min(v.config.material_ids),
+                         reverse=True)
+
+        cset = ConductivitySet()
+        active = set()
+        scale = 1.0 / (cfg.chi_m * cfg.membrane_capacitance)
+        for vol in self.volumes:
+            for mat in vol.config.material_ids:
+                cset.add(mat, vol.config.sigma_l * scale, vol.config.sigma_t * scale,
+                         vol.config.sigma_n * scale, vol.config.disabled)
+                if not vol.config.disabled:
+                    active.add(mat)
+        self.active_materials = active
+        inactive = self.space.inactive_dof_mask(cset.disabled_ids())
+        self.inactive = inactive
+
+        # nodal initial state (smaller material ID wins at interfaces)
+        u0 = np.zeros(n)
+        rest = np.zeros(n)
+        thr = np.zeros(n)
+        w0 = {}
+        for vol in by_desc:
+            state, trace = vol.initial_cell_state(cfg.bdf_order)
+            w0[id(vol)] = np.broadcast_to(state.w, (vol.dofs.size, vol.num_vars))
+            u0[vol.dofs] = state.u
+            rest[vol.dofs] = vol.rest_u
+            thr[vol.dofs] = vol.threshold
+            if trace is not None and vol.config.zero_d_csv_path:
+                from .outputs import write_zero_d_trace
+
+                write_zero_d_trace(vol.config.zero_d_csv_path, trace)
+        u0[inactive] = rest[inactive]
+        self.rest_field = rest
+        self.thresholds = thr
+
+        # operators
+        rows, table = _sigma_table(self.space, cset)
+        dm = DeviceMesh(mesh, cfg.fibers)
+        K_local, M_local = dm.element_matrices(rows, table)
+        include_k = torch.from_numpy((rows >= 0).astype(np.uint8)).cuda()
+        include_m = dm.include_mask(active)
+        self.lift_volumes = [v for v in self.volumes if not v.config.disabled]
+        if len(self.lift_volumes) > N.MAX_LIFT:
+            raise ConfigError("Physical constants and models",
+                              f"at most {N.MAX_LIFT} conducting volumes")
+        lift_includes = [None if set(v.config.material_ids) == active
+                         else dm.include_mask(v.config.material_ids)
+                         for v in self.lift_volumes]
+        orders = sorted({min(k + 1, cfg.bdf_order) for k in range(cfg.bdf_order)})
+        lattice = detect_lattice(mesh) if operator in ("auto", "stencil") else None
+        args = (K_local, M_local, include_k, include_m, lift_includes, inactive,
+                rest, thr, cfg.dt, orders)
+        self.op = None
+        if lattice is not None:
+            try:
+                self.op = StencilOperator(dm, lattice, *args)
+            except OverflowError:
+                if operator == "stencil":
+                    raise
+        if self.op is None:
+            self.op = CsrOperator(dm, self.space, *args)
+        del K_local, M_local, dm
+
+        # device state
+        ld = _pad(n)
+        self.ld = ld
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.u_ring = torch.zeros((RING_SLOTS, ld), **f64)
+        self.u_ring[0, :n] = torch.from_numpy(u0).cuda()
+        self.head = 0
+        self.u_fill = 1
+        for vol in self.volumes:
+            lw = _pad(vol.dofs.size)
+            vol.ldw = lw
+            vol.w_ring = torch.zeros((RING_SLOTS, vol.num_vars, lw), **f64)
+            vol.w_ring[0, :, :vol.dofs.size] = torch.from_numpy(
+                np.ascontiguousarray(w0[id(vol)].T)).cuda()
+            vol.w_fill = 1
+            vol.d_dofs = (None if (vol.dofs.size == n and vol.dofs[-1] == n - 1)
+                          else torch.from_numpy(vol.dofs.astype(np.int32)).cuda())
+        self.currents = torch.zeros((max(len(self.lift_volumes), 1), ld), **f64)
+        self.combo = torch.zeros(ld, **f64)
+        self.fused_prep = (len(self.lift_volumes) == 1
+                           and self.lift_volumes[0].d_dofs is None)
+
+        # stimuli: time-independent profiles (simulation.py:374-382)
+        self._impulses = []
+        coords = self.space.dof_coords
+        profiles = []
+        for protocol in cfg.stimuli:
+            for i in range(len(protocol.sites)):
+                prof = protocol.spatial_factor(coords, i) / cfg.membrane_capacitance
+                prof[inactive] = 0.0
+                self._impulses.append((protocol, i))
+                profiles.append(prof)
+        if len(profiles) > 64:
+            raise ConfigError("Stimulus", "at most 64 impulses")
+        self.profiles = (torch.from_numpy(np.ascontiguousarray(
+            np.stack(profiles))).cuda() if profiles else None)
+
+        # activation (simulation.py:384-388)
+        self.act_time = torch.full((n,), ACTIVATION_SENTINEL, **f64)
+        self.best_slope = torch.full((n,), -np.inf, **f64)
+        self.frozen = torch.from_numpy(inactive.astype(np.uint8)).cuda()
+
+        # solver workspace and logs
+        from .linalg import CgWorkspace
+
+        self.ws = CgWorkspace(n)
+        self.iter_log = torch.zeros(1024, dtype=torch.int32, device="cuda")
+        self.relres_log = torch.zeros(1024, dtype=torch.float64, device="cuda")
+        self.clamps = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self._log_base = 0
+        self._pending = []          # (step_index, head_before, time_before)
+        self._max_seen = 0
+        self._last_iters = 0
+        self.launches = 0
+
+    # -- per-step launch sequence ---------------------------------------------
+
+    def _active_mask(self, t_next):
+        mask = 0
+        for k, (protocol, i) in enumerate(self._impulses):
+            if protocol.window_active(i, t_next):
+                mask |= 1 << k
+        return mask
+
+    def _ensure_log(self, slot):
+        import torch
+
+        if slot >= self.iter_log.numel():
+            grow = max(slot + 1, 2 * self.iter_log.numel())
+            il = torch.zeros(grow, dtype=torch.int32, device="cuda")
+            rl = torch.zeros(grow, dtype=torch.float64, device="cuda")
+            il[: self.iter_log.numel()] = self.iter_log
+            rl[: self.relres_log.numel()] = self.relres_log
+            self.iter_log, self.relres_log = il, rl
+
+    def enqueue_step(self, events=None):
+        """Launch one step; no host synchronisation.
+
+        `events`: optional (after_ionic, after_solve) CUDA events recorded on
+        the launch stream (bench.py's per-kernel timing).
+        """
+        import torch
+
+        cfg = self.config
+        order = min(self.step_index + 1, cfg.bdf_order)
+        t_next = self.time + self.dt
+        mask = self._active_mask(t_next)
+        stream = N.stream_handle()
+        lib = N.lib()
+        head = self.head
+        nslot = (head + 1) % RING_SLOTS
+        timed = self.timed
+        if timed:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+
+        ia = N.TissueIonicArgs()
+        ia.u_ring = N.ptr(self.u_ring)
+        ia.ldu = self.ld
+        ia.ring_slots = RING_SLOTS
+        ia.head = head
+        ia.order = order
+        ia.dt = self.dt
+        ia.clamp_count = N.ptr(self.clamps)
+        ia.combo = N.ptr(self.combo)
+        ia.profiles = N.ptr(self.profiles)
+        ia.ldp = self.n
+        ia.active_mask = mask
+        ia.n_impulses = len(self._impulses)
+        ia.status = N.ptr(self.ws.status)
+        if not self.fused_prep:
+            ia.n = self.n
+            ia.prep = 1
+            N.check(lib.mdx_tissue_prep(N.C.byref(ia), stream), "mdx_tissue_prep")
+            self.launches += 1
+        for v, vol in enumerate(self.lift_volumes):
+            ia.n = vol.dofs.size
+            ia.dofs = N.ptr(vol.d_dofs)
+            ia.w_ring = N.ptr(vol.w_ring)
+            ia.ldw = vol.ldw
+            ia.i_out = N.ptr(self.currents[v])
+            ia.prep = 1 if self.fused_prep else 0
+            Ph, Pp = N.host_doubles(vol.packed)
+            N.check(lib.mdx_tissue_ionic(vol.module.MODEL_ID, N.C.byref(ia), Pp,
+                                         int(Ph.size), stream), "mdx_tissue_ionic")
+            self.launches += 1
+        if timed:
+            ev[1].record()
+        if events is not None:
+            events[0].record()
+
+        op = self.op
+        a = N.CgArgs()
+        a.op = op.operator()
+        a.a_val = N.ptr(op.a_tables[order])
+        a.dinv = N.ptr(op.dinv[order])
+        a.m_val = N.ptr(op.d_m)
+        a.combo = N.ptr(self.combo)
+        a.n_lift = len(self.lift_volumes)
+        a.step = self.step_index
+        for v in range(len(self.lift_volumes)):
+            a.lift_val[v] = N.ptr(op.d_lift[v])
+            a.lift_cur[v] = N.ptr(self.currents[v])
+        a.inactive = N.ptr(op.d_inactive)
+        a.rest = N.ptr(op.d_rest)
+        a.thr = N.ptr(op.d_thr)
+        a.x = N.ptr(self.u_ring[nslot])
+        a.u_prev = N.ptr(self.u_ring[head])
+        a.act_time = N.ptr(self.act_time)
+        a.best_slope = N.ptr(self.best_slope)
+        a.frozen = N.ptr(self.frozen)
+        a.t_next = t_next
+        a.dt = self.dt
+        a.tol = cfg.linear_solver.tolerance
+        a.max_iter = cfg.linear_solver.max_iterations
+        self.ws.fill(a)
+        slot = self.step_index - self._log_base
+        self._ensure_log(slot)
+        a.iters_out = self.iter_log.data_ptr() + 4 * slot
+        a.relres_out = self.relres_log.data_ptr() + 8 * slot
+        N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.npt_hint, stream), "mdx_pcg_solve")
+        self.launches += 1
+        if events is not None:
+            events[1].record()
+        if timed:
+            ev[2].record()
+            self.timer.device_span("Ionic model update", ev[0], ev[1])
+            self.timer.device_span("Linear solver", ev[1], ev[2])
+
+        self._pending.append((self.step_index, head, self.time))
+        self.head = nslot
+        self.u_fill = min(self.u_fill + 1, 3)
+        for vol in self.lift_volumes:
+            vol.w_fill = min(vol.w_fill + 1, 3)
+        self.step_index += 1
+        self.time = t_next
+
+    def sync(self):
+        """Wait for the device; raise the reference exception of a failed step."""
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        st = int(self.ws.status.item())
+        if self._pending:
+            first = self._pending[0][0]
+            last = self._pending[-1][0]
+            its = self.iter_log[first - self._log_base: last - self._log_base + 1]
+            if st:
+                fail = int(self.ws.fail_step.item())
+                its = its[: max(fail - first, 0)]
+            if its.numel():
+                self._max_seen = max(self._max_seen, int(its.max().item()))
+                self._last_iters = int(its[-1].item())
+        if st:
+            fail = int(self.ws.fail_step.item())
+            for (k, head, t) in self._pending:
+                if k == fail:
+                    self.step_index, self.head, self.time = k, head, t
+                    break
+            self._pending = []
+            rel = float(self.relres_log[fail - self._log_base].item())
+            its = int(self.iter_log[fail - self._log_base].item())
+            if st & N.STATUS_DIVERGED:
+                raise SolverDivergence(-its, rel)
+            raise NonFiniteSolution("linear solve produced non-finite entries")
+        self._pending = []
+
+    def step(self, return_potential=True):
+        """Advance one step (TissueSolver.step, simulation.py:425-483).
+
+        Returns the new potential as a numpy array (drop-in semantics, one
+        synchronisation) or, with return_potential=False, None without
+        synchronising.
+        """
+        self.enqueue_step()
+        if not return_potential:
+            return None
+        self.sync()
+        return self.potential
+
+    def advance(self, steps):
+        """Enqueue `steps` steps back to back, then synchronise once."""
+        for _ in range(steps):
+            self.enqueue_step()
+        self.sync()
+
+    # -- state access ---------------------------------------------------------
+
+    @property
+    def potential_device(self):
+        return self.u_ring[self.head, : self.n]
+
+    @property
+    def potential(self):
+        return self.potential_device.cpu().numpy()
+
+    @property
+    def last_iterations(self):
+        if self._pending:
+            self.sync()
+        return self._last_iters
+
+    @property
+    def max_iterations_seen(self):
+        if self._pending:
+            self.sync()
+        return self._max_seen
+
+    def iterations_log(self):
+        """Per-step CG iteration counts since construction (or restore)."""
+        if self._pending:
+            self.sync()
+        k = self.step_index - self._log_base
+        return self.iter_log[:k].cpu().numpy().astype(np.int64)
+
+    @property
+    def activation_time(self):
+        return self.act_time.cpu().numpy()
+
+    @property
+    def activation_map(self):
+        fr = self.frozen.cpu().numpy().astype(bool)
+        return np.where(fr, self.act_time.cpu().numpy(), ACTIVATION_SENTINEL)
+
+    def fully_activated(self):
+        fr = self.frozen.cpu().numpy().astype(bool)
+        return bool(fr[~self.inactive].all())
+
+    def clamp_total(self):
+        return int(self.clamps.item())
+
+    def volume_state(self, k, index=0):
+        """AoS (ndofs, nv) ionic state of volume k, `index` steps back."""
+        vol = self.volumes[k]
+        slot = (self.head - index) % RING_SLOTS if not vol.config.disabled else 0
+        return vol.w_ring[slot, :, : vol.dofs.size].t().contiguous().cpu().numpy()
+
+    # -- checkpointing (simulation.py:518-631), reference byte format --------
+
+    def checkpoint_payload(self):
+        if self._pending:
+            self.sync()
+        n = self.n
+        parts = [struct.pack("<IQ", CHECKPOINT_VERSION, n),
+                 struct.pack("<Qd", self.step_index, self.time),
+                 struct.pack("<I", self.u_fill)]
+        for k in range(self.u_fill):
+            slot = (self.head - k) % RING_SLOTS
+            parts.append(self.u_ring[slot, :n].cpu().numpy().tobytes())
+        parts.append(self.act_time.cpu().numpy().tobytes())
+        parts.append(self.best_slope.cpu().numpy().tobytes())
+        parts.append(self.frozen.cpu().numpy().astype(np.uint8).tobytes())
+        parts.append(struct.pack("<I", len(self.volumes)))
+        for vol in self.volumes:
+            label = vol.config.label.encode("utf-8")
+            parts.append(struct.pack("<I", len(label)))
+            parts.append(label)
+            fill = 1 if vol.config.disabled else vol.w_fill
+            parts.append(struct.pack("<IQI", vol.num_vars, vol.dofs.size, fill))
+            for k in range(fill):
+                slot = 0 if vol.config.disabled else (self.head - k) % RING_SLOTS
+                aos = vol.w_ring[slot, :, : vol.dofs.size].t().contiguous()
+                parts.append(aos.cpu().numpy().tobytes())
+        return b"".join(parts)
+
+    def restore(self, payload):
+        import torch
+
+        if self._pending:
+            self.sync()
+        version, n = struct.unpack_from("<IQ", payload, 0)
+        if version != CHECKPOINT_VERSION:
+            raise VersionMismatch(f"checkpoint version {version}, expected "
+                                  f"{CHECKPOINT_VERSION}")
+        if n != self.n:
+            raise DofCountMismatch(f"checkpoint has {n} DOFs, mesh has {self.n}")
+        off = struct.calcsize("<IQ")
+        step_index, t = struct.unpack_from("<Qd", payload, off)
+        off += struct.calcsize("<Qd")
+
+        def take(count, dtype=np.float64):
+            nonlocal off
+            arr = np.frombuffer(payload, dtype=dtype, count=count, offset=off).copy()
+            off += count * np.dtype(dtype).itemsize
+            return arr
+
+        (fill,) = struct.unpack_from("<I", payload, off)
+        off += 4
+        us = [take(n) for _ in range(fill)]
+        act = take(n)
+        best = take(n)
+        frozen = take(n, np.uint8)
+        (nvols,) = struct.unpack_from("<I", payload, off)
+        off += 4
+        if nvols != len(self.volumes):
+            raise CorruptFile(f"checkpoint has {nvols} volumes, config has "
+                              f"{len(self.volumes)}")
+        vol_states = []
+        for vol in self.volumes:
+            (ll,) = struct.unpack_from("<I", payload, off)
+            off += 4
+            label = payload[off: off + ll].decode("utf-8")
+            off += ll
+            if label != vol.config.label:
+                raise CorruptFile(f"checkpoint volume {label!r} does not match "
+                                  f"{vol.config.label!r}")
+            nv, nd, wf = struct.unpack_from("<IQI", payload, off)
+            off += struct.calcsize("<IQI")
+            if nv != vol.num_vars or nd != vol.dofs.size:
+                raise DofCountMismatch(f"checkpoint volume {label!r} shape mismatch")
+            vol_states.append([take(nd * nv).reshape(nd, nv) for _ in range(wf)])
+        # newest first -> slots head, head-1, ...
+        self.head = 0
+        for k, u in enumerate(us):
+            self.u_ring[(-k) % RING_SLOTS, :n] = torch.from_numpy(u).cuda()
+        self.u_fill = fill
+        for vol, states in zip(self.volumes, vol_states):
+            for k, w in enumerate(states):
+                vol.w_ring[(-k) % RING_SLOTS, :, : vol.dofs.size] = \
+                    torch.from_numpy(np.ascontiguousarray(w.T)).cuda()
+            vol.w_fill = len(states)
+        self.act_time.copy_(torch.from_numpy(act))
+        self.best_slope.copy_(torch.from_numpy(best))
+        self.frozen.copy_(torch.from_numpy(frozen))
+        self.step_index, self.time = int(step_index), float(t)
+        self._log_base = self.step_index
+        self.ws.status.zero_()
+
+
+CHECKPOINT_MAGIC = b"MHEP"
+CHECKPOINT_VERSION = 1
+
+
+def save_checkpoint(solver, path):
+    payload = solver.checkpoint_payload()
+    with open(path, "wb") as fh:
+        fh.write(CHECKPOINT_MAGIC)
+        fh.write(payload)
+        fh.write(struct.pack("<I", zlib.crc32(payload) & 0xFFFFFFFF))
+
+
+def load_checkpoint(path):
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < len(CHECKPOINT_MAGIC) + 4 or not blob.startswith(CHECKPOINT_MAGIC):
+        raise CorruptFile(f"{path} is not a checkpoint file")
+    payload = blob[len(CHECKPOINT_MAGIC): -4]
+    (stored,) = struct.unpack("<I", blob[-4:])
+    if zlib.crc32(payload) & 0xFFFFFFFF != stored:
+        raise CorruptFile(f"{path} failed its checksum")
+    return payload
+
+
+# ---------------------------------------------------------------------------
+# Run loop (simulation.py:634-716)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class RunReport:
+    activation_times: np.ndarray
+    final_potential: np.ndarray
+    timings: dict
+    steps: int
+    max_cg_iterations: int
+    csv_path: str = None
+    vtk_paths: tuple = ()
+    solver: TissueSolver = None
+    rows: list = None
+
+
+def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
+    """Execute a configured simulation to its final time on the device.
+
+    Steps are enqueued back to back; the host synchronises only to record an
+    output row (every `output.stride` steps, a 2+P-value read-back) or to
+    test full activation.
+    """
+    import torch
+
+    solver = TissueSolver(config, **solver_kw)
+    if resume_from is not None:
+        solver.restore(load_checkpoint(resume_from))
+    n_steps = int(round(config.final_time / config.dt))
+    out = getattr(config, "output", None) or OutputConfig()
+    rows, vtk_paths = [], []
+    probes = [nearest_node(config.mesh, p) for p in out.probe_points]
+    probe_idx = torch.tensor(probes, dtype=torch.int64, device="cuda") if probes else None
+
+    def record():
+        with solver.timer.section("Other"):
+            if out.enable_csv or not out.enable_field_output:
+                u = solver.potential_device
+                mm = torch.aminmax(u)
+                vals = [mm.min.reshape(1), mm.max.reshape(1)]
+                if probe_idx is not None:
+                    vals.append(u[probe_idx])
+                row = torch.cat(vals).cpu().numpy()
+                rows.append((solver.time, *row.tolist()))
+            if out.enable_field_output:
+                path = f"{out.field_stem}_{solver.step_index:06d}.vtk"
+                write_vtk(path, config.mesh, {"transmembrane_potential": solver.potential})
+                vtk_paths.append(path)
+
+    if solver.step_index == 0:
+        record()
+    while solver.step_index < n_steps:
+        solver.enqueue_step()
+        k = solver.step_index
+        if k % out.stride == 0 or k == n_steps:
+            solver.sync()
+            record()
+        if stop_when_fully_activated and solver.fully_activated():
+            break
+    solver.sync()
+    with solver.timer.section("Other"):
+        csv_path = None
+        if out.enable_csv:
+            write_csv(out.csv_path, rows, probe_count=len(probes))
+            csv_path = out.csv_path
+        act_cfg = getattr(config, "activation", None)
+        if act_cfg is not None and act_cfg.enabled:
+            write_vtk(act_cfg.path, config.mesh, {"activation_time": solver.activation_map})
+            vtk_paths.append(act_cfg.path)
+        ck = getattr(config, "checkpoint", None)
+        if ck is not None and ck.enabled:
+            save_checkpoint(solver, ck.path)
+    return RunReport(
+        activation_times=solver.activation_map,
+        final_potential=solver.potential.copy(),
+        timings=dict(solver.timer.totals),
+        steps=solver.step_index,
+        max_cg_iterations=solver.max_iterations_seen,
+        csv_path=csv_path,
+        vtk_paths=tuple(vtk_paths),
+        solver=solver,
+        rows=rows,
+    )

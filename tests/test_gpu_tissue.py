@@ -1,0 +1,338 @@
+"""CUDA tissue path vs the reference (golden fixtures) and the CPU oracle.
+
+Parity bar (BASELINE.json north_star): fp64 potential traces within relative
+L2 1e-6, activation times within one dt, CG iteration counts within +-1 per
+step.  Operators are bit-identical to the reference (hash-pinned).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+# ---------------------------------------------------------------------------
+# operators
+# ---------------------------------------------------------------------------
+
+MESHES = {
+    "unit_hex": ((1.0, 1.0, 1.0), 1.0, "Hex8", (0, 0.0, 0.0)),
+    "hex27": ((1e-3, 1e-3, 1e-3), 0.5e-3, "Hex8", (0, 60.0, -60.0)),
+    "tet_slab": ((2e-3, 3e-3, 4e-3), 0.5e-3, "Tet4", (2, 60.0, -60.0)),
+    "hex_slab": ((2e-3, 3e-3, 4e-3), 0.5e-3, "Hex8", (2, 60.0, -60.0)),
+    "cfg0_hex": ((20e-3, 7e-3, 3e-3), 0.5e-3, "Hex8", (2, 0.0, 0.0)),
+    "cfg0_tet": ((20e-3, 7e-3, 3e-3), 0.5e-3, "Tet4", (2, 0.0, 0.0)),
+}
+
+
+def _mesh(name):
+    from paper_2308_01651_b200.geometry import ElementKind, SlabSpec, build_slab_mesh, slab_fiber_field
+
+    ext, h, kind, fib = MESHES[name]
+    mesh = build_slab_mesh(SlabSpec(ext, h, ElementKind(kind)))
+    two = name in ("tet_slab", "hex_slab")
+    if two:
+        mats = mesh.material_ids.copy()
+        mats[mesh.nodes[mesh.elements].mean(axis=1)[:, 2] > 2e-3] = 2
+        mesh = mesh.with_materials(mats)
+    return mesh, slab_fiber_field(mesh, *fib), two
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_device_assembly_bit_identical(golden, name):
+    from paper_2308_01651_b200.fem import ConductivitySet, FeSpace, assemble_mass, assemble_stiffness
+
+    g = golden("operators")
+    mesh, fibers, two = _mesh(name)
+    space = FeSpace(mesh)
+    cs = ConductivitySet().add(1, 1.2e-4, 3e-5, 1.5e-5)
+    if two:
+        cs.add(2, 2e-4, 1e-5, 1e-5)
+    K = assemble_stiffness(space, cs, fibers)
+    M = assemble_mass(space)
+    assert _sha(K.indptr.astype(np.int64)) == str(g[f"{name}_K_indptr_sha"])
+    assert _sha(K.indices.astype(np.int32)) == str(g[f"{name}_K_indices_sha"])
+    assert _sha(K.data) == str(g[f"{name}_K_data_sha"])
+    assert _sha(M.data) == str(g[f"{name}_M_data_sha"])
+    if two:
+        assert _sha(assemble_mass(space, {1}).data) == str(g[f"{name}_M1_data_sha"])
+    if f"{name}_K_data" in g:
+        np.testing.assert_array_equal(K.data, g[f"{name}_K_data"])
+
+
+def test_unit_hex_closed_forms():
+    """tests/test_fem.py:71-89: M_ii = 1/27, K_ii = 1/3, K diagonals -1/12."""
+    from paper_2308_01651_b200.fem import ConductivitySet, FeSpace, assemble_mass, assemble_stiffness
+
+    mesh, fibers, _ = _mesh("unit_hex")
+    space = FeSpace(mesh)
+    M = assemble_mass(space).toarray()
+    K = assemble_stiffness(space, ConductivitySet().add(1, 1.0, 1.0, 1.0), fibers).toarray()
+    np.testing.assert_allclose(np.diag(M), 1.0 / 27.0, rtol=1e-14)
+    np.testing.assert_allclose(np.diag(K), 1.0 / 3.0, rtol=1e-14)
+    np.testing.assert_allclose(K.sum(axis=1), 0.0, atol=1e-15)
+    assert K[0, 6] == pytest.approx(-1.0 / 12.0, rel=1e-14)
+
+
+def test_csr_matvec_bitwise_vs_oracle():
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200.fem import ConductivitySet, FeSpace, assemble_stiffness
+    from paper_2308_01651_b200.linalg import csr_matvec
+
+    mesh, fibers, _ = _mesh("cfg0_tet")
+    K = assemble_stiffness(FeSpace(mesh), ConductivitySet().add(1, 1e-4, 2e-5, 1e-5), fibers)
+    x = np.random.default_rng(3).standard_normal(K.shape[0])
+    y = np.empty(K.shape[0])
+    csr_matvec(K.indptr, K.indices, K.data, x, y)
+    np.testing.assert_array_equal(y, O.Csr.from_scipy(K).matvec(x))
+
+
+def test_jacobi_cg_known_systems(golden):
+    import scipy.sparse as sp
+
+    from paper_2308_01651_b200.errors import SolverDivergence
+    from paper_2308_01651_b200.fem import ConductivitySet, FeSpace, assemble_mass, assemble_stiffness
+    from paper_2308_01651_b200.geometry import ElementKind, SlabSpec, build_slab_mesh, slab_fiber_field
+    from paper_2308_01651_b200.linalg import JacobiCg, solve_cg
+
+    x, it, _ = solve_cg(sp.identity(5, format="csr"), np.array([1.0, -2, 3, 0.5, 0]))
+    assert np.allclose(x, [1, -2, 3, 0.5, 0]) and it <= 1
+    A2 = sp.csr_matrix(np.array([[4.0, 1.0], [1.0, 3.0]]))
+    x, _, _ = solve_cg(A2, np.array([1.0, 2.0]), tolerance=1e-14)
+    np.testing.assert_allclose(x, [1 / 11, 7 / 11], atol=1e-13)
+    x, it, _ = solve_cg(A2, np.zeros(2))
+    assert (x == 0).all() and it == 0
+
+    g = golden("cg_kat")
+    mesh = build_slab_mesh(SlabSpec((3e-3, 7e-3, 20e-3), 0.5e-3, ElementKind.HEX8))
+    space = FeSpace(mesh)
+    K = assemble_stiffness(space, ConductivitySet().add(1, 0.95298e-4, 0.12576e-4,
+                                                       0.12576e-4),
+                           slab_fiber_field(mesh, 0, 0.0, 0.0))
+    A = ((1.5 / 5e-5) * assemble_mass(space) + K).tocsr()
+    assert _sha(A.data) == str(g["A_data_sha"])
+    solver = JacobiCg(A, 1e-10, 2000)
+    x, it, rel = solver.solve(g["b"])
+    assert abs(it - int(g["iters"])) <= 1
+    assert _rel(x, g["x"]) < 1e-9
+    assert np.linalg.norm(g["b"] - A @ x) <= 1e-10 * np.linalg.norm(g["b"])
+    _, it0, _ = solver.solve(g["b"], initial_guess=g["x"])
+    assert it0 == 0
+    xw, itw, _ = solver.solve(g["b"], initial_guess=g["x0"])
+    assert abs(itw - int(g["itersw"])) <= 1 and _rel(xw, g["xw"]) < 1e-9
+    x1, i1, r1 = JacobiCg(A, 1e-10, 2000).solve(g["b"])
+    x2, i2, r2 = JacobiCg(A, 1e-10, 2000).solve(g["b"])
+    assert i1 == i2 and r1 == r2 and np.array_equal(x1, x2)   # deterministic
+    with pytest.raises(SolverDivergence) as err:
+        solve_cg(A, g["b"], tolerance=1e-15, max_iterations=2)
+    assert err.value.iterations == 2
+    with pytest.raises(ValueError):
+        JacobiCg(sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 2.0]])))
+
+
+def test_stencil_operator_matches_csr_bitwise(ns):
+    """Class-table stencil apply == reference CSR matvec, bit for bit."""
+    import torch
+
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import _native as N, configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    for cfg in (configs.config0(ns), configs.config3(ns, h=0.5e-3)):
+        st = TissueSolver(cfg, operator="stencil")
+        cs = TissueSolver(cfg, operator="csr")
+        assert st.op.kind == N.OP_STENCIL27 and cs.op.kind == N.OP_CSR
+        x = torch.from_numpy(np.random.default_rng(5).standard_normal(st.n)).cuda()
+        for order in st.op.a_tables:
+            ys = []
+            for s in (st, cs):
+                a = N.CgArgs()
+                a.op = s.op.operator()
+                a.a_val = N.ptr(s.op.a_tables[order])
+                y = torch.empty_like(x)
+                N.check(N.lib().mdx_spmv(N.C.byref(a), N.ptr(x), N.ptr(y),
+                                         N.stream_handle()))
+                ys.append(y.cpu().numpy())
+            np.testing.assert_array_equal(ys[0], ys[1])
+        orc = O.OracleTissue(cfg)
+        orc._system(1.5)
+        np.testing.assert_array_equal(orc.A.matvec(x.cpu().numpy()), ys[1])
+
+
+# ---------------------------------------------------------------------------
+# tissue runs vs reference goldens
+# ---------------------------------------------------------------------------
+
+
+def _run_against(g, cfg, steps, operator="auto"):
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    s = TissueSolver(cfg, operator=operator)
+    probes = g["probes"]
+    pu = np.empty((steps, probes.size))
+    for k in range(steps):
+        u = s.step()
+        pu[k] = u[probes]
+    return s, pu
+
+
+def _check(s, pu, g, dt, steps, trace_tol=1e-6):
+    its = s.iterations_log()
+    ref_its = g["iters"][:steps]
+    assert np.abs(its - ref_its).max() <= 1, np.flatnonzero(its != ref_its)
+    rel = _rel(pu, g["probe_u"][:steps])
+    assert rel < trace_tol, rel
+    act, ref = s.activation_map, g["activation"]
+    both = (act >= 0) & (ref >= 0)
+    assert np.array_equal(act >= 0, ref >= 0)
+    assert np.abs(act[both] - ref[both]).max() <= dt * (1 + 1e-9)
+    return its, rel
+
+
+def test_cfg0_bo_full_run(golden, ns):
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg0")
+    s, pu = _run_against(g, configs.config0(ns), 800)
+    its, rel = _check(s, pu, g, 5e-5, 800)
+    assert rel < 1e-9               # reduction-order noise only
+    assert (its == g["iters"]).mean() > 0.99
+    assert _rel(s.potential, g["final_u"]) < 1e-9
+    np.testing.assert_allclose(s.volume_state(0), g["final_w0"], rtol=1e-8, atol=1e-10)
+
+
+def test_cfg0_csr_path_matches(golden, ns):
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg0")
+    s, pu = _run_against(g, configs.config0(ns), 300, operator="csr")
+    _check(s, pu, g, 5e-5, 300)
+
+
+def test_tet_mesh_run(golden, ns):
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_tet")
+    s, pu = _run_against(g, configs.config0(ns, kind="Tet4"), 400)
+    _check(s, pu, g, 5e-5, 400)
+
+
+def test_ttp06_slab(golden, ns):
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_ttp_h05")
+    s, pu = _run_against(g, configs.config2(ns, h=0.5e-3), 2000)
+    _check(s, pu, g, 2e-5, 2000)
+    assert _rel(s.potential, g["final_u"]) < 1e-8
+
+
+def test_cfg3_scar_full_500ms(golden, ns):
+    """Three volumes (duplicated interface states), two stimuli, 25,000 steps."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    g = golden("tissue_cfg3_h05")
+    steps = int(g["steps"])
+    s = TissueSolver(configs.config3(ns, h=0.5e-3))
+    probes = g["probes"]
+    pu = np.empty((steps, probes.size))
+    chunk = 500
+    done = 0
+    while done < steps:
+        m = min(chunk, steps - done)
+        for _ in range(m):
+            s.enqueue_step()
+        s.sync()
+        done += m
+        pu[done - 1] = s.potential[probes]
+    its = s.iterations_log()
+    assert np.abs(its - g["iters"]).max() <= 1
+    ref = g["probe_u"][chunk - 1::chunk]
+    assert _rel(pu[chunk - 1::chunk], ref) < 1e-6
+    assert _rel(s.potential, g["final_u"]) < 1e-6
+    act, ra = s.activation_map, g["activation"]
+    both = (act >= 0) & (ra >= 0)
+    assert np.array_equal(act >= 0, ra >= 0)
+    assert np.abs(act[both] - ra[both]).max() <= 2e-5 * (1 + 1e-9)
+
+
+def test_cfg2_full_size_head(golden, ns):
+    """Config 2 at full size (442,401 nodes): first 40 steps vs the reference."""
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg2_head")
+    s, pu = _run_against(g, configs.config2(ns), 40)
+    its = s.iterations_log()
+    assert np.abs(its - g["iters"]).max() <= 1
+    assert _rel(pu, g["probe_u"]) < 1e-9
+    sub = int(g["subsample"])
+    assert _rel(s.potential[::sub], g["final_u_sub"]) < 1e-9
+    assert s.op.ncls == 27          # uniform slab: interior + 26 boundary classes
+
+
+def test_checkpoint_format_and_cross_restore(golden, ns):
+    """Restore the REFERENCE's checkpoint (step 400) and continue to 800."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    g = golden("tissue_cfg0")
+    cfg = configs.config0(ns)
+    s = TissueSolver(cfg)
+    s.restore(g["payload_400"].tobytes())
+    assert s.step_index == 400
+    s.advance(400)
+    assert _rel(s.potential, g["final_u"]) < 1e-9
+    # our payload has the reference layout and round-trips
+    ref_payload = g["payload_400"].tobytes()
+    s2 = TissueSolver(cfg)
+    s2.advance(400)
+    mine = s2.checkpoint_payload()
+    assert len(mine) == len(ref_payload)
+    assert mine[:12] == ref_payload[:12]
+    s3 = TissueSolver(cfg)
+    s3.restore(mine)
+    assert s3.checkpoint_payload() == mine
+
+
+def test_divergence_is_raised_and_state_rolls_back(ns):
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.errors import SolverDivergence
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = configs.config0(ns, h=1e-3)
+    cfg.linear_solver.max_iterations = 3
+    s = TissueSolver(cfg)
+    for _ in range(5):
+        s.enqueue_step()
+    with pytest.raises(SolverDivergence) as err:
+        s.sync()
+    assert err.value.iterations == 3
+    assert s.step_index == 0 and s.time == 0.0
+
+
+def test_oracle_live_parity_random_config(ns):
+    """A seeded two-material slab, BDF3, checked against the live oracle."""
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = configs.config3(ns, h=1e-3, seed=7)
+    cfg.bdf_order = 3
+    s = TissueSolver(cfg)
+    o = O.OracleTissue(cfg)
+    for _ in range(150):
+        s.enqueue_step()
+        o.step()
+    s.sync()
+    assert np.abs(s.iterations_log() - np.array(o.iters)).max() <= 1
+    assert _rel(s.potential, o.potential) < 1e-9
