@@ -145,7 +145,9 @@ typedef struct mdx_cg_args {
   const double* thr;       /* activation threshold */
   /* vectors */
   double* x;             /* in: warm start (u_EXT); out: solution */
-  double* p;             /* work, n doubles */
+  double* p;             /* work vectors, n doubles each */
+  double* q;
+  double* r;
   /* activation map (tissue; act_time NULL = skip) */
   const double* u_prev;
   double* act_time;
@@ -163,8 +165,8 @@ typedef struct mdx_cg_args {
   int32_t* fail_step;    /* receives `step` when status is raised */
 } mdx_cg_args;
 
-/* npt_hint: minimum nodes per thread (0 = automatic) */
-int mdx_pcg_solve(const mdx_cg_args* args, int tissue, int npt_hint, void* stream);
+/* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */
+int mdx_pcg_solve(const mdx_cg_args* args, int tissue, int blocks_hint, void* stream);
 /* y = A x with the same row arithmetic (csr_matvec, linalg.py:17-23) */
 int mdx_spmv(const mdx_cg_args* args, const double* x, double* y, void* stream);
 
@@ -195,10 +197,17 @@ int mdx_scatter_csr(int64_t n, int nl, const int32_t* elements, const int64_t* i
                     double* data, void* stream);
 int mdx_stencil_rows(int nx, int ny, int nz, const uint8_t* include, const double* local,
                      double* rows, void* stream);
-int mdx_hash_rows(int64_t n, int width, const double* rows, unsigned long long* out,
-                  void* stream);
-int mdx_verify_classes(int64_t n, int width, const double* rows, const uint16_t* cls,
-                       const int64_t* rep, unsigned long long* mismatches, void* stream);
+/* Node classes of the stencil operator: rows are [nblk x 27 coefficients |
+ * nextra exact columns]; coefficients are compared to 36 bits relative to
+ * each block's largest entry (element matrices built from node coordinates
+ * differ in the last bits between analytically equal elements).
+ * mismatches[0] counts rows off their class representative, mismatches[1]
+ * receives the largest relative deviation (as the bits of a double). */
+int mdx_hash_rows(int64_t n, int nblk, int nextra, const double* rows,
+                  unsigned long long* out, void* stream);
+int mdx_verify_classes(int64_t n, int nblk, int nextra, const double* rows,
+                       const uint16_t* cls, const int64_t* rep,
+                       unsigned long long* mismatches, void* stream);
 /* A = c*M + K entrywise (simulation.py:398) */
 int mdx_combine_system(int64_t m, double c, const double* M, const double* K, double* A,
                        void* stream);

@@ -58,6 +58,7 @@ class CgArgs(C.Structure):
         ("m_val", _p), ("combo", _p), ("n_lift", _i32), ("step", _i32),
         ("lift_val", _p * MAX_LIFT), ("lift_cur", _p * MAX_LIFT),
         ("inactive", _p), ("rest", _p), ("thr", _p), ("x", _p), ("p", _p),
+        ("q", _p), ("r", _p),
         ("u_prev", _p), ("act_time", _p), ("best_slope", _p), ("frozen", _p),
         ("t_next", _d), ("dt", _d), ("tol", _d), ("max_iter", _i32),
         ("partials_capacity", _i32), ("partials", _p), ("barrier", _p),
@@ -106,8 +107,8 @@ _SIGNATURES = {
     "mdx_scatter_csr": ([_i64, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
                         C.c_int),
     "mdx_stencil_rows": ([C.c_int, C.c_int, C.c_int, _p, _p, _p, _p], C.c_int),
-    "mdx_hash_rows": ([_i64, C.c_int, _p, _p, _p], C.c_int),
-    "mdx_verify_classes": ([_i64, C.c_int, _p, _p, _p, _p, _p], C.c_int),
+    "mdx_hash_rows": ([_i64, C.c_int, C.c_int, _p, _p, _p], C.c_int),
+    "mdx_verify_classes": ([_i64, C.c_int, C.c_int, _p, _p, _p, _p, _p], C.c_int),
     "mdx_combine_system": ([_i64, _d, _p, _p, _p, _p], C.c_int),
     "mdx_pace_cells": ([C.c_int, C.POINTER(PaceArgs), _p, C.c_int, _p],
                        C.c_int),

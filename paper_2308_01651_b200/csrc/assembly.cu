@@ -188,41 +188,81 @@ stencil_rows(int nx, int ny, int nz, const uint8_t* __restrict__ include,
   }
 }
 
-// FNV-1a over the raw bits of each row (class detection).
-__global__ void hash_rows(int64_t n, int width, const double* __restrict__ rows,
+// Row classes for the stencil operator.  The reference assembles every
+// element from its own node coordinates, so rows that are analytically equal
+// differ in the last bits (i*h is not exactly uniform); classes therefore
+// group rows that agree to QUANT_BITS bits relative to the largest entry of
+// each 27-wide block.  Trailing `nextra` columns (flags, rest potential,
+// threshold) must match exactly.
+constexpr int QUANT_BITS = 36;
+
+__device__ __forceinline__ int block_exponent(const double* r) {
+  double m = 0.0;
+  for (int k = 0; k < 27; ++k) m = fmax(m, fabs(r[k]));
+  return m > 0.0 ? ilogb(m) : -2000;
+}
+
+__device__ __forceinline__ void fnv(unsigned long long& h, unsigned long long v) {
+  for (int byte = 0; byte < 8; ++byte) {
+    h ^= (v >> (8 * byte)) & 0xffull;
+    h *= 1099511628211ull;
+  }
+}
+
+__global__ void hash_rows(int64_t n, int nblk, int nextra, const double* __restrict__ rows,
                           unsigned long long* __restrict__ out) {
+  const int width = 27 * nblk + nextra;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long h = 1469598103934665603ull;
-    const unsigned long long* r =
-        reinterpret_cast<const unsigned long long*>(rows + i * (int64_t)width);
-    for (int k = 0; k < width; ++k) {
-      unsigned long long v = r[k];
-      for (int byte = 0; byte < 8; ++byte) {
-        h ^= (v >> (8 * byte)) & 0xffull;
-        h *= 1099511628211ull;
+    const double* r = rows + i * (int64_t)width;
+    for (int b = 0; b < nblk; ++b) {
+      const double* blk = r + 27 * b;
+      const int e = block_exponent(blk);
+      fnv(h, (unsigned long long)(e + 4096));
+      for (int k = 0; k < 27; ++k) {
+        const double qv = e > -2000 ? rint(ldexp(blk[k], QUANT_BITS - e)) : 0.0;
+        fnv(h, (unsigned long long)(long long)qv);
       }
     }
+    for (int k = 27 * nblk; k < width; ++k) fnv(h, __double_as_longlong(r[k]));
     out[i] = h;
   }
 }
 
-// Counts rows whose bits differ from their class representative's.
-__global__ void verify_classes(int64_t n, int width, const double* __restrict__ rows,
+// Counts rows farther than 4 quanta from their class representative (or
+// with different exact columns); also records the largest relative
+// deviation |row - rep| / max|rep block| in dev_bits (as ordered bits).
+__global__ void verify_classes(int64_t n, int nblk, int nextra,
+                               const double* __restrict__ rows,
                                const uint16_t* __restrict__ cls,
                                const int64_t* __restrict__ rep,
                                unsigned long long* __restrict__ mismatches) {
+  const int width = 27 * nblk + nextra;
   unsigned long long bad = 0;
+  double worst = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long* a =
-        reinterpret_cast<const unsigned long long*>(rows + i * (int64_t)width);
-    const unsigned long long* b =
-        reinterpret_cast<const unsigned long long*>(rows + rep[cls[i]] * (int64_t)width);
-    for (int k = 0; k < width; ++k)
-      if (a[k] != b[k]) { ++bad; break; }
+    const double* a = rows + i * (int64_t)width;
+    const double* b = rows + rep[cls[i]] * (int64_t)width;
+    bool ok = true;
+    for (int blk = 0; blk < nblk; ++blk) {
+      double m = 0.0;
+      for (int k = 0; k < 27; ++k) m = fmax(m, fabs(b[27 * blk + k]));
+      const double tol = m > 0.0 ? ldexp(m, 2 - QUANT_BITS) : 0.0;
+      for (int k = 0; k < 27; ++k) {
+        const double d = fabs(a[27 * blk + k] - b[27 * blk + k]);
+        if (d > tol) ok = false;
+        if (m > 0.0) worst = fmax(worst, d / m);
+      }
+    }
+    for (int k = 27 * nblk; k < width; ++k)
+      if (__double_as_longlong(a[k]) != __double_as_longlong(b[k])) ok = false;
+    if (!ok) ++bad;
   }
   if (bad) atomicAdd(mismatches, bad);
+  // non-negative doubles order like their bit patterns
+  atomicMax(mismatches + 1, (unsigned long long)__double_as_longlong(worst));
 }
 
 // y = c*M + K entrywise (scipy's scalar-times-matrix then matrix add, each
@@ -288,18 +328,19 @@ int mdx_stencil_rows(int nx, int ny, int nz, const uint8_t* include, const doubl
   return check_launch("mdx_stencil_rows");
 }
 
-int mdx_hash_rows(int64_t n, int width, const double* rows, unsigned long long* out,
-                  void* stream) {
+int mdx_hash_rows(int64_t n, int nblk, int nextra, const double* rows,
+                  unsigned long long* out, void* stream) {
   if (n <= 0) return MDX_OK;
-  hash_rows<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(n, width, rows, out);
+  hash_rows<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(n, nblk, nextra, rows, out);
   return check_launch("mdx_hash_rows");
 }
 
-int mdx_verify_classes(int64_t n, int width, const double* rows, const uint16_t* cls,
-                       const int64_t* rep, unsigned long long* mismatches, void* stream) {
+int mdx_verify_classes(int64_t n, int nblk, int nextra, const double* rows,
+                       const uint16_t* cls, const int64_t* rep,
+                       unsigned long long* mismatches, void* stream) {
   if (n <= 0) return MDX_OK;
-  verify_classes<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(n, width, rows, cls, rep,
-                                                                  mismatches);
+  verify_classes<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(n, nblk, nextra, rows, cls,
+                                                                  rep, mismatches);
   return check_launch("mdx_verify_classes");
 }
 

@@ -346,11 +346,11 @@ def ici_lift(per_subdomain_mass, nodal_currents):
 
 def detect_lattice(mesh):
     """(nx, ny, nz) if `mesh` is numbered exactly like a structured hex slab."""
+    if _kind_of(mesh) is not ElementKind.HEX8:
+        return None
     lat = getattr(mesh, "lattice", None)
     if lat is not None:
         return tuple(lat)
-    if _kind_of(mesh) is not ElementKind.HEX8:
-        return None
     nodes = mesh.nodes
     axes = [np.unique(nodes[:, d]) for d in range(3)]
     nx, ny, nz = (len(a) - 1 for a in axes)

@@ -36,6 +36,10 @@ def _layout(W, nv):
         raise ValueError(f"state array must have shape (N, {nv}), got {tuple(W.shape)}")
     s0, s1 = (W.stride() if _is_cuda_tensor(W)
               else tuple(s // W.itemsize for s in W.strides))
+    if nv == 1:
+        s1 = 0          # a single variable: the variable stride is never used
+    if W.shape[0] == 1:
+        s0 = 0
     return s0, s1
 
 

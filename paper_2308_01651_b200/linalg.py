@@ -33,6 +33,8 @@ class CgWorkspace:
         self.partials = torch.zeros(self.capacity * 4, dtype=torch.float64, device="cuda")
         self.barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
         self.p = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.q = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.r = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.iters = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.relres = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -43,6 +45,8 @@ class CgWorkspace:
         a.partials = N.ptr(self.partials)
         a.barrier = N.ptr(self.barrier)
         a.p = N.ptr(self.p)
+        a.q = N.ptr(self.q)
+        a.r = N.ptr(self.r)
         a.iters_out = N.ptr(self.iters)
         a.relres_out = N.ptr(self.relres)
         a.status = N.ptr(self.status)

@@ -9,10 +9,15 @@ threshold, and 1/A_ii (`/root/reference/pkg/src/monodomain/simulation.py:
 `StencilOperator` (structured hex slabs): every node row has at most 27
 entries at fixed lattice offsets, and rows repeat: a uniform slab has 27
 distinct row patterns (interior, faces, edges, corners); a slab with a scar
-has a few hundred.  The device computes every node's row bits from the
-element matrices, hashes them, and the host groups equal rows into classes.
-A node then costs 2 bytes (its class id) and the operator streams no matrix
-data at all - the "matrix-free" apply with exactly the reference's entries.
+has a few hundred.  The device computes every node's row from the element
+matrices, hashes it (coefficients to 36 bits relative to the row block's
+largest entry: the reference integrates each element from its own node
+coordinates, so analytically equal rows differ in the last bits), and the
+host groups rows into classes whose table row is one representative node's
+exact row.  A node then costs 2 bytes (its class id) and the operator
+streams no matrix data - a matrix-free apply whose entries match the
+reference's to ~1e-15 relative (`max_rel_dev`).  `CsrOperator` is the
+bit-exact alternative (`TissueSolver(..., operator="csr")`).
 
 `CsrOperator` (any mesh): the reference pattern with device-assembled values.
 """
@@ -54,9 +59,9 @@ class StencilOperator:
             inactive.astype(np.float64), rest.astype(np.float64),
             thr.astype(np.float64)])).cuda()
         key = torch.cat([rows_k, rows_m, *lift_rows, extra], dim=1).contiguous()
-        width = key.shape[1]
+        nblk = 2 + len(lift_rows)
         hashes = torch.empty(self.n, dtype=torch.int64, device="cuda")
-        N.check(N.lib().mdx_hash_rows(self.n, width, N.ptr(key), N.ptr(hashes),
+        N.check(N.lib().mdx_hash_rows(self.n, nblk, 3, N.ptr(key), N.ptr(hashes),
                                       N.stream_handle()), "mdx_hash_rows")
         h = hashes.cpu().numpy()
         uniq, first, inverse = np.unique(h, return_index=True, return_inverse=True)
@@ -65,12 +70,15 @@ class StencilOperator:
         self.ncls = int(uniq.size)
         self.cls = torch.from_numpy(inverse.astype(np.uint16)).cuda()
         rep = torch.from_numpy(first.astype(np.int64)).cuda()
-        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
-        N.check(N.lib().mdx_verify_classes(self.n, width, N.ptr(key), N.ptr(self.cls),
+        bad = torch.zeros(2, dtype=torch.int64, device="cuda")
+        N.check(N.lib().mdx_verify_classes(self.n, nblk, 3, N.ptr(key), N.ptr(self.cls),
                                            N.ptr(rep), N.ptr(bad), N.stream_handle()),
                 "mdx_verify_classes")
-        if int(bad.item()):
-            raise OverflowError("stencil row hash collision")
+        badh = bad.cpu().numpy()
+        if int(badh[0]):
+            raise OverflowError(f"{int(badh[0])} stencil rows off their class")
+        # largest |row - class row| / max|class row| over all nodes and blocks
+        self.max_rel_dev = float(badh[1:2].view(np.float64)[0])
         tab = key[rep].cpu().numpy()
         nl = len(lift_rows)
         self.tab_k = np.ascontiguousarray(tab[:, 0:27])

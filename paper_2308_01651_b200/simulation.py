@@ -296,12 +296,12 @@ def _pad(n):
 class TissueSolver:
     """Owns the device operators and state; advances the coupled system."""
 
-    def __init__(self, config, operator="auto", npt_hint=0, timed=False):
+    def __init__(self, config, operator="auto", blocks_hint=0, timed=False):
         validate_config(config)
         self.config = config
         self.timer = SectionTimer()
         self.timed = timed
-        self.npt_hint = npt_hint
+        self.blocks_hint = blocks_hint
         with self.timer.section("Initialization"):
             self._initialize(operator)
 
@@ -544,7 +544,7 @@ class TissueSolver:
         self._ensure_log(slot)
         a.iters_out = self.iter_log.data_ptr() + 4 * slot
         a.relres_out = self.relres_log.data_ptr() + 8 * slot
-        N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.npt_hint, stream), "mdx_pcg_solve")
+        N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.blocks_hint, stream), "mdx_pcg_solve")
         self.launches += 1
         if events is not None:
             events[1].record()

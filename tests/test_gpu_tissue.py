@@ -140,8 +140,10 @@ def test_jacobi_cg_known_systems(golden):
         JacobiCg(sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 2.0]])))
 
 
-def test_stencil_operator_matches_csr_bitwise(ns):
-    """Class-table stencil apply == reference CSR matvec, bit for bit."""
+def test_stencil_operator_matches_csr(ns):
+    """Class-table stencil apply vs the bit-exact CSR operator: the class rows
+    are one representative node's exact row, so they differ from a node's own
+    row by the reference's coordinate round-off only (<= 1e-13 relative)."""
     import torch
 
     from oracle import monodomain_oracle as O
@@ -163,10 +165,23 @@ def test_stencil_operator_matches_csr_bitwise(ns):
                 N.check(N.lib().mdx_spmv(N.C.byref(a), N.ptr(x), N.ptr(y),
                                          N.stream_handle()))
                 ys.append(y.cpu().numpy())
-            np.testing.assert_array_equal(ys[0], ys[1])
+            absx = torch.abs(x)
+            scale = []
+            for s in (cs,):
+                a = N.CgArgs()
+                a.op = s.op.operator()
+                absA = torch.abs(s.op.a_tables[order])
+                a.a_val = N.ptr(absA)
+                y = torch.empty_like(x)
+                N.check(N.lib().mdx_spmv(N.C.byref(a), N.ptr(absx), N.ptr(y),
+                                         N.stream_handle()))
+                scale = y.cpu().numpy()
+            assert (np.abs(ys[0] - ys[1]) <= 1e-13 * scale).all()
+        assert st.op.max_rel_dev < 1e-13
+        assert st.op.ncls <= 200
         orc = O.OracleTissue(cfg)
         orc._system(1.5)
-        np.testing.assert_array_equal(orc.A.matvec(x.cpu().numpy()), ys[1])
+        np.testing.assert_array_equal(orc.A.matvec(x.cpu().numpy()), ys[1])  # CSR: bitwise
 
 
 # ---------------------------------------------------------------------------
@@ -192,6 +207,8 @@ def _check(s, pu, g, dt, steps, trace_tol=1e-6):
     assert np.abs(its - ref_its).max() <= 1, np.flatnonzero(its != ref_its)
     rel = _rel(pu, g["probe_u"][:steps])
     assert rel < trace_tol, rel
+    if steps != int(g["steps"]):
+        return its, rel
     act, ref = s.activation_map, g["activation"]
     both = (act >= 0) & (ref >= 0)
     assert np.array_equal(act >= 0, ref >= 0)
