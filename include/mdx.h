@@ -120,7 +120,7 @@ typedef struct mdx_operator {
   int64_t n;             /* rows = nodes */
   int32_t nx1, ny1, nz1; /* stencil: nodes per axis (x fastest) */
   int32_t _pad;
-  const uint16_t* cls;   /* stencil: class id of every node */
+  const uint32_t* meta;  /* stencil: class id | neighbour mask << 16, per node */
   const int64_t* indptr; /* csr */
   const int32_t* indices;
   int64_t nnz;

@@ -13,7 +13,9 @@ import numpy as np
 
 from .errors import NativeUnavailable
 
-_LIB_PATH = Path(__file__).resolve().parent / "libmdx.so"
+import os
+
+_LIB_PATH = Path(os.environ.get("MDX_LIB", Path(__file__).resolve().parent / "libmdx.so"))
 _lib = None
 
 MDX_OK = 0
@@ -47,7 +49,7 @@ class TissueIonicArgs(C.Structure):
 class Operator(C.Structure):
     _fields_ = [
         ("kind", _i32), ("ncls", _i32), ("n", _i64), ("nx1", _i32),
-        ("ny1", _i32), ("nz1", _i32), ("_pad", _i32), ("cls", _p),
+        ("ny1", _i32), ("nz1", _i32), ("_pad", _i32), ("meta", _p),
         ("indptr", _p), ("indices", _p), ("nnz", _i64),
     ]
 

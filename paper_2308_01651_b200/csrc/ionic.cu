@@ -12,6 +12,10 @@
 #include "common.cuh"
 #include "ionic_models.cuh"
 
+#ifndef MDX_IONIC_MINB
+#define MDX_IONIC_MINB 1
+#endif
+
 namespace mdx {
 
 static thread_local char g_err[512];
@@ -141,7 +145,7 @@ __device__ __forceinline__ double combine(const double (&x)[ORDER], const double
 // x0 = u_EXT into the u ring's next slot, so no separate nodal pass runs.
 // ---------------------------------------------------------------------------
 template <class M, int ORDER>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, MDX_IONIC_MINB)
 tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
   if (a.status && *(volatile const int32_t*)a.status) return;
   const Bdf b = bdf_of(ORDER);

@@ -69,6 +69,13 @@ class StencilOperator:
             raise OverflowError(f"{uniq.size} stencil classes exceed {MAX_CLASSES}")
         self.ncls = int(uniq.size)
         self.cls = torch.from_numpy(inverse.astype(np.uint16)).cuda()
+        # per-node operator word: class id | neighbour-validity mask << 16
+        k, j, i = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1),
+                              indexing="ij")
+        i, j, k = i.ravel(), j.ravel(), k.ravel()
+        mask = ((i > 0) * 1 | (i < nx) * 2 | (j > 0) * 4 | (j < ny) * 8 | (k > 0) * 16
+                | (k < nz) * 32).astype(np.uint32)
+        self.meta = torch.from_numpy(inverse.astype(np.uint32) | (mask << 16)).cuda()
         rep = torch.from_numpy(first.astype(np.int64)).cuda()
         bad = torch.zeros(2, dtype=torch.int64, device="cuda")
         N.check(N.lib().mdx_verify_classes(self.n, nblk, 3, N.ptr(key), N.ptr(self.cls),
@@ -120,7 +127,7 @@ class StencilOperator:
         op.ncls = self.ncls
         op.n = self.n
         op.nx1, op.ny1, op.nz1 = (d + 1 for d in self.lattice)
-        op.cls = N.ptr(self.cls)
+        op.meta = N.ptr(self.meta)
         return op
 
     def device_bytes(self):

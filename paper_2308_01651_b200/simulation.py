@@ -438,6 +438,7 @@ class TissueSolver:
         self._max_seen = 0
         self._last_iters = 0
         self.launches = 0
+        self._build_launch_args()
 
     # -- per-step launch sequence ---------------------------------------------
 
@@ -459,6 +460,55 @@ class TissueSolver:
             rl[: self.relres_log.numel()] = self.relres_log
             self.iter_log, self.relres_log = il, rl
 
+    def _build_launch_args(self):
+        """ctypes argument blocks built once; per step only scalars change."""
+        cfg = self.config
+        self._stream = N.stream_handle()
+        self._ionic_args = []
+        base = dict(u_ring=N.ptr(self.u_ring), ldu=self.ld, ring_slots=RING_SLOTS,
+                    dt=self.dt, clamp_count=N.ptr(self.clamps), combo=N.ptr(self.combo),
+                    profiles=N.ptr(self.profiles), ldp=self.n,
+                    n_impulses=len(self._impulses), status=N.ptr(self.ws.status))
+        if not self.fused_prep:
+            ia = N.TissueIonicArgs(**base)
+            ia.n = self.n
+            ia.prep = 1
+            self._prep_args = ia
+        for v, vol in enumerate(self.lift_volumes):
+            ia = N.TissueIonicArgs(**base)
+            ia.n = vol.dofs.size
+            ia.dofs = N.ptr(vol.d_dofs)
+            ia.w_ring = N.ptr(vol.w_ring)
+            ia.ldw = vol.ldw
+            ia.i_out = N.ptr(self.currents[v])
+            ia.prep = 1 if self.fused_prep else 0
+            Ph, Pp = N.host_doubles(vol.packed)
+            self._ionic_args.append((vol.module.MODEL_ID, ia, Ph, Pp))
+        op = self.op
+        a = N.CgArgs()
+        a.op = op.operator()
+        a.m_val = N.ptr(op.d_m)
+        a.combo = N.ptr(self.combo)
+        a.n_lift = len(self.lift_volumes)
+        for v in range(len(self.lift_volumes)):
+            a.lift_val[v] = N.ptr(op.d_lift[v])
+            a.lift_cur[v] = N.ptr(self.currents[v])
+        a.inactive = N.ptr(op.d_inactive)
+        a.rest = N.ptr(op.d_rest)
+        a.thr = N.ptr(op.d_thr)
+        a.act_time = N.ptr(self.act_time)
+        a.best_slope = N.ptr(self.best_slope)
+        a.frozen = N.ptr(self.frozen)
+        a.dt = self.dt
+        a.tol = cfg.linear_solver.tolerance
+        a.max_iter = cfg.linear_solver.max_iterations
+        self.ws.fill(a)
+        self._cg_args = a
+        self._a_ptr = {k: N.ptr(v) for k, v in op.a_tables.items()}
+        self._dinv_ptr = {k: N.ptr(v) for k, v in op.dinv.items()}
+        self._slot_ptr = [N.ptr(self.u_ring[s]) for s in range(RING_SLOTS)]
+        self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
+
     def enqueue_step(self, events=None):
         """Launch one step; no host synchronisation.
 
@@ -467,83 +517,45 @@ class TissueSolver:
         """
         import torch
 
-        cfg = self.config
-        order = min(self.step_index + 1, cfg.bdf_order)
+        order = min(self.step_index + 1, self.config.bdf_order)
         t_next = self.time + self.dt
-        mask = self._active_mask(t_next)
-        stream = N.stream_handle()
+        mask = self._active_mask(t_next) if self._impulses else 0
         lib = N.lib()
+        stream = self._stream
         head = self.head
         nslot = (head + 1) % RING_SLOTS
         timed = self.timed
         if timed:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record()
-
-        ia = N.TissueIonicArgs()
-        ia.u_ring = N.ptr(self.u_ring)
-        ia.ldu = self.ld
-        ia.ring_slots = RING_SLOTS
-        ia.head = head
-        ia.order = order
-        ia.dt = self.dt
-        ia.clamp_count = N.ptr(self.clamps)
-        ia.combo = N.ptr(self.combo)
-        ia.profiles = N.ptr(self.profiles)
-        ia.ldp = self.n
-        ia.active_mask = mask
-        ia.n_impulses = len(self._impulses)
-        ia.status = N.ptr(self.ws.status)
         if not self.fused_prep:
-            ia.n = self.n
-            ia.prep = 1
+            ia = self._prep_args
+            ia.head, ia.order, ia.active_mask = head, order, mask
             N.check(lib.mdx_tissue_prep(N.C.byref(ia), stream), "mdx_tissue_prep")
             self.launches += 1
-        for v, vol in enumerate(self.lift_volumes):
-            ia.n = vol.dofs.size
-            ia.dofs = N.ptr(vol.d_dofs)
-            ia.w_ring = N.ptr(vol.w_ring)
-            ia.ldw = vol.ldw
-            ia.i_out = N.ptr(self.currents[v])
-            ia.prep = 1 if self.fused_prep else 0
-            Ph, Pp = N.host_doubles(vol.packed)
-            N.check(lib.mdx_tissue_ionic(vol.module.MODEL_ID, N.C.byref(ia), Pp,
-                                         int(Ph.size), stream), "mdx_tissue_ionic")
+        for model_id, ia, Ph, Pp in self._ionic_args:
+            ia.head, ia.order, ia.active_mask = head, order, mask
+            N.check(lib.mdx_tissue_ionic(model_id, N.C.byref(ia), Pp, int(Ph.size), stream),
+                    "mdx_tissue_ionic")
             self.launches += 1
         if timed:
             ev[1].record()
         if events is not None:
             events[0].record()
 
-        op = self.op
-        a = N.CgArgs()
-        a.op = op.operator()
-        a.a_val = N.ptr(op.a_tables[order])
-        a.dinv = N.ptr(op.dinv[order])
-        a.m_val = N.ptr(op.d_m)
-        a.combo = N.ptr(self.combo)
-        a.n_lift = len(self.lift_volumes)
+        a = self._cg_args
+        a.a_val = self._a_ptr[order]
+        a.dinv = self._dinv_ptr[order]
         a.step = self.step_index
-        for v in range(len(self.lift_volumes)):
-            a.lift_val[v] = N.ptr(op.d_lift[v])
-            a.lift_cur[v] = N.ptr(self.currents[v])
-        a.inactive = N.ptr(op.d_inactive)
-        a.rest = N.ptr(op.d_rest)
-        a.thr = N.ptr(op.d_thr)
-        a.x = N.ptr(self.u_ring[nslot])
-        a.u_prev = N.ptr(self.u_ring[head])
-        a.act_time = N.ptr(self.act_time)
-        a.best_slope = N.ptr(self.best_slope)
-        a.frozen = N.ptr(self.frozen)
+        a.x = self._slot_ptr[nslot]
+        a.u_prev = self._slot_ptr[head]
         a.t_next = t_next
-        a.dt = self.dt
-        a.tol = cfg.linear_solver.tolerance
-        a.max_iter = cfg.linear_solver.max_iterations
-        self.ws.fill(a)
         slot = self.step_index - self._log_base
-        self._ensure_log(slot)
-        a.iters_out = self.iter_log.data_ptr() + 4 * slot
-        a.relres_out = self.relres_log.data_ptr() + 8 * slot
+        if slot >= self.iter_log.numel():
+            self._ensure_log(slot)
+            self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
+        a.iters_out = self._log_ptrs[0] + 4 * slot
+        a.relres_out = self._log_ptrs[1] + 8 * slot
         N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.blocks_hint, stream), "mdx_pcg_solve")
         self.launches += 1
         if events is not None:
