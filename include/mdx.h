@@ -148,6 +148,7 @@ typedef struct mdx_cg_args {
   double* p;             /* work vectors, n doubles each */
   double* q;
   double* r;
+  double* z;             /* variant 1 only: z = D^-1 r, read by the neighbours */
   /* activation map (tissue; act_time NULL = skip) */
   const double* u_prev;
   double* act_time;
@@ -158,11 +159,13 @@ typedef struct mdx_cg_args {
   int32_t max_iter;
   int32_t partials_capacity; /* blocks the partials buffer can hold */
   double* partials;      /* [partials_capacity][4] */
-  unsigned int* barrier; /* [2], zero-initialised once, reused */
+  unsigned long long* barrier; /* grid-barrier counter, zero-initialised, reused */
   int32_t* iters_out;    /* iterations (reference convention: -max_iter) */
   double* relres_out;
   int32_t* status;       /* nonzero on entry => no-op; bit0 diverged, bit1 non-finite */
   int32_t* fail_step;    /* receives `step` when status is raised */
+  int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2) */
+  int32_t _pad1;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */

@@ -60,12 +60,12 @@ class CgArgs(C.Structure):
         ("m_val", _p), ("combo", _p), ("n_lift", _i32), ("step", _i32),
         ("lift_val", _p * MAX_LIFT), ("lift_cur", _p * MAX_LIFT),
         ("inactive", _p), ("rest", _p), ("thr", _p), ("x", _p), ("p", _p),
-        ("q", _p), ("r", _p),
+        ("q", _p), ("r", _p), ("z", _p),
         ("u_prev", _p), ("act_time", _p), ("best_slope", _p), ("frozen", _p),
         ("t_next", _d), ("dt", _d), ("tol", _d), ("max_iter", _i32),
         ("partials_capacity", _i32), ("partials", _p), ("barrier", _p),
         ("iters_out", _p), ("relres_out", _p), ("status", _p),
-        ("fail_step", _p),
+        ("fail_step", _p), ("variant", _i32), ("_pad1", _i32),
     ]
 
 

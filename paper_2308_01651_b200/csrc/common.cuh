@@ -65,27 +65,23 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
 }
 
 // Software grid barrier for a launch whose blocks are all co-resident
-// (cooperative launch). bar[0] counts arrivals, bar[1] is the generation.
-// The gpu-scope fences make every write issued before the barrier visible
-// to every block after it (and invalidate stale L1 lines).
-__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int nblocks) {
-  if (nblocks == 1) {
-    __syncthreads();
-    return;
-  }
+// (cooperative launch).  bar is a monotonic 64-bit arrival counter whose
+// value is a multiple of the grid size between barriers: a block arrives
+// with one release atomic and spins (acquire loads) until the count reaches
+// the end of its epoch.  The gpu-scope fences make every write issued before
+// the barrier visible to every block after it (and invalidate stale L1).
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned int nblocks) {
   __syncthreads();
+  if (nblocks == 1) return;
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = bar + 1;
-    const unsigned int gen = *vgen;
     __threadfence();
-    const unsigned int arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) __nanosleep(20);
-    }
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+    const unsigned long long target = (old / nblocks + 1) * nblocks;
+    unsigned long long cur;
+    do {
+      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+    } while (cur < target);
     __threadfence();
   }
   __syncthreads();

@@ -31,10 +31,11 @@ class CgWorkspace:
             max_blocks = props.multi_processor_count * 8
         self.capacity = int(max_blocks)
         self.partials = torch.zeros(self.capacity * 4, dtype=torch.float64, device="cuda")
-        self.barrier = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.barrier = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.p = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.q = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.r = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.z = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.iters = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.relres = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -47,6 +48,7 @@ class CgWorkspace:
         a.p = N.ptr(self.p)
         a.q = N.ptr(self.q)
         a.r = N.ptr(self.r)
+        a.z = N.ptr(self.z)
         a.iters_out = N.ptr(self.iters)
         a.relres_out = N.ptr(self.relres)
         a.status = N.ptr(self.status)

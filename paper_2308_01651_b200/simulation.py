@@ -296,12 +296,15 @@ def _pad(n):
 class TissueSolver:
     """Owns the device operators and state; advances the coupled system."""
 
-    def __init__(self, config, operator="auto", blocks_hint=0, timed=False):
+    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=1):
         validate_config(config)
         self.config = config
         self.timer = SectionTimer()
         self.timed = timed
         self.blocks_hint = blocks_hint
+        # 1: q carried by recurrence (2 grid syncs per CG iteration); 0: the
+        # reference recurrences verbatim (3 syncs).  Same iterates up to rounding.
+        self.cg_variant = cg_variant
         with self.timer.section("Initialization"):
             self._initialize(operator)
 
@@ -503,6 +506,7 @@ class TissueSolver:
         a.tol = cfg.linear_solver.tolerance
         a.max_iter = cfg.linear_solver.max_iterations
         self.ws.fill(a)
+        a.variant = self.cg_variant
         self._cg_args = a
         self._a_ptr = {k: N.ptr(v) for k, v in op.a_tables.items()}
         self._dinv_ptr = {k: N.ptr(v) for k, v in op.dinv.items()}

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--h", type=float, default=None)
     ap.add_argument("--operator", default="auto")
     ap.add_argument("--blocks", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=1)
     args = ap.parse_args()
 
     import torch
@@ -33,7 +34,8 @@ def main():
     kw = {} if args.h is None else {"h": args.h}
     cfg = {"0": configs.config0, "2": configs.config2, "3": configs.config3}[args.config](
         ns, **kw)
-    s = TissueSolver(cfg, operator=args.operator, blocks_hint=args.blocks)
+    s = TissueSolver(cfg, operator=args.operator, blocks_hint=args.blocks,
+                     cg_variant=args.variant)
     for _ in range(args.warmup):
         s.enqueue_step()
     s.sync()

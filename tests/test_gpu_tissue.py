@@ -353,3 +353,32 @@ def test_oracle_live_parity_random_config(ns):
     s.sync()
     assert np.abs(s.iterations_log() - np.array(o.iters)).max() <= 1
     assert _rel(s.potential, o.potential) < 1e-9
+
+
+def test_cfg0_reference_cg_recurrences(golden, ns):
+    """cg_variant=0 runs the reference's recurrences verbatim (q = A p)."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    g = golden("tissue_cfg0")
+    s = TissueSolver(configs.config0(ns), cg_variant=0)
+    probes = g["probes"]
+    pu = np.empty((800, probes.size))
+    for k in range(800):
+        pu[k] = s.step()[probes]
+    _check(s, pu, g, 5e-5, 800)
+
+
+def test_single_block_and_multi_block_grids_agree(ns):
+    """The same solve on 1 block and on many blocks (grid barrier path)."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = configs.config0(ns)
+    runs = []
+    for blocks in (1, 7):
+        s = TissueSolver(cfg, blocks_hint=blocks)
+        s.advance(100)
+        runs.append((s.iterations_log(), s.potential))
+    assert np.abs(runs[0][0] - runs[1][0]).max() <= 1
+    assert _rel(runs[0][1], runs[1][1]) < 1e-10
