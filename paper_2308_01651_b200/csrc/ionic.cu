@@ -13,7 +13,7 @@
 #include "ionic_models.cuh"
 
 #ifndef MDX_IONIC_MINB
-#define MDX_IONIC_MINB 1
+#define MDX_IONIC_MINB 3
 #endif
 
 namespace mdx {
@@ -345,6 +345,7 @@ static typename M::Params load_params(const double* P, int np, int* err) {
     return p;
   }
   memcpy(p.p, P, sizeof(double) * M::NP);
+  M::derive(p);
   *err = MDX_OK;
   return p;
 }
