@@ -1,0 +1,85 @@
+"""Summarise ncu reports (.ncu-rep) and a launch-list CSV into profiles/.
+
+    python scripts/summarize_ncu.py <out.md> <launches.csv> <rep1> [<rep2> ...]
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe % active"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}, vals[hdr.index("Kernel Name")]
+
+
+def stalls(d):
+    st = []
+    for k, (v, _) in d.items():
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith(
+                "_per_issue_active.ratio"):
+            try:
+                st.append((float(v), k[len("smsp__average_warps_issue_stalled_"):
+                                       -len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    return sorted(st, reverse=True)[:6]
+
+
+def main():
+    out, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    lines = ["# ncu summary", ""]
+    for rep in reps:
+        d, name = raw(rep)
+        lines += [f"## `{name[:110]}`", "", f"report: `{rep}`", "",
+                  "| metric | value | unit |", "|---|---|---|"]
+        for key, label in METRICS:
+            if key in d:
+                v, u = d[key]
+                lines.append(f"| {label} (`{key}`) | {v} | {u} |")
+        lines += ["", "top stall reasons (warps per issued instruction): " +
+                  ", ".join(f"{n} {v:.2f}" for v, n in stalls(d)), ""]
+    # launch list: share of device time per kernel
+    rows = list(csv.DictReader(l for l in open(launches) if not l.startswith("==")))
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        k = r["Kernel Name"].split("(")[0]
+        v = float(r["Metric Value"].replace(",", ""))
+        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r["Metric Unit"], 1.0)
+        tot[k] += v * scale
+        cnt[k] += 1
+    all_t = sum(tot.values())
+    lines += ["## launch list (ncu, --clock-control none, serialised, cold cache)", "",
+              "| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        lines.append(f"| `{k[:80]}` | {cnt[k]} | {v:.1f} | {v / all_t:.1%} |")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
