@@ -148,7 +148,12 @@ typedef struct mdx_cg_args {
   double* p;             /* work vectors, n doubles each */
   double* q;
   double* r;
-  double* z;             /* variant 1 only: z = D^-1 r, read by the neighbours */
+  double* z;             /* variants 1, 2 */
+  /* variant 2 (pipelined CG) only: w = A u, s = A p, m = D^-1 w (2n: two
+     buffers alternating between iterations) */
+  double* w;
+  double* s;
+  double* m;
   /* activation map (tissue; act_time NULL = skip) */
   const double* u_prev;
   double* act_time;
@@ -164,7 +169,8 @@ typedef struct mdx_cg_args {
   double* relres_out;
   int32_t* status;       /* nonzero on entry => no-op; bit0 diverged, bit1 non-finite */
   int32_t* fail_step;    /* receives `step` when status is raised */
-  int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2) */
+  int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2);
+                            2: pipelined PCG (1 reduction/iter) */
   int32_t _pad1;
 } mdx_cg_args;
 

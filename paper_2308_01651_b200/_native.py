@@ -60,7 +60,8 @@ class CgArgs(C.Structure):
         ("m_val", _p), ("combo", _p), ("n_lift", _i32), ("step", _i32),
         ("lift_val", _p * MAX_LIFT), ("lift_cur", _p * MAX_LIFT),
         ("inactive", _p), ("rest", _p), ("thr", _p), ("x", _p), ("p", _p),
-        ("q", _p), ("r", _p), ("z", _p),
+        ("q", _p), ("r", _p), ("z", _p), ("w", _p), ("s", _p),
+        ("m", _p),
         ("u_prev", _p), ("act_time", _p), ("best_slope", _p), ("frozen", _p),
         ("t_next", _d), ("dt", _d), ("tol", _d), ("max_iter", _i32),
         ("partials_capacity", _i32), ("partials", _p), ("barrier", _p),

@@ -36,6 +36,9 @@ class CgWorkspace:
         self.q = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.r = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.z = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.w = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.s = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        self.m = torch.zeros(2 * max(n, 1), dtype=torch.float64, device="cuda")
         self.iters = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.relres = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -49,6 +52,9 @@ class CgWorkspace:
         a.q = N.ptr(self.q)
         a.r = N.ptr(self.r)
         a.z = N.ptr(self.z)
+        a.w = N.ptr(self.w)
+        a.s = N.ptr(self.s)
+        a.m = N.ptr(self.m)
         a.iters_out = N.ptr(self.iters)
         a.relres_out = N.ptr(self.relres)
         a.status = N.ptr(self.status)

@@ -296,14 +296,15 @@ def _pad(n):
 class TissueSolver:
     """Owns the device operators and state; advances the coupled system."""
 
-    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=1):
+    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=2):
         validate_config(config)
         self.config = config
         self.timer = SectionTimer()
         self.timed = timed
         self.blocks_hint = blocks_hint
-        # 1: q carried by recurrence (2 grid syncs per CG iteration); 0: the
-        # reference recurrences verbatim (3 syncs).  Same iterates up to rounding.
+        # CG recurrences (csrc/solver.cu): 0 = the reference's verbatim (3 grid
+        # syncs per iteration), 1 = q by recurrence (2), 2 = pipelined PCG (1).
+        # Same Krylov iterates up to rounding; all checked against the goldens.
         self.cg_variant = cg_variant
         with self.timer.section("Initialization"):
             self._initialize(operator)

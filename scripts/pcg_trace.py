@@ -18,7 +18,7 @@ def main():
 
     cfg = configs.config2(configs.this_package())
     blocks = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-    s = TissueSolver(cfg, blocks_hint=blocks)
+    s = TissueSolver(cfg, blocks_hint=blocks, cg_variant=int(sys.argv[2]) if len(sys.argv) > 2 else 2)
     for _ in range(6):
         s.enqueue_step()
     s.sync()

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--h", type=float, default=None)
     ap.add_argument("--operator", default="auto")
     ap.add_argument("--blocks", type=int, default=0)
-    ap.add_argument("--variant", type=int, default=1)
+    ap.add_argument("--variant", type=int, default=2)
     args = ap.parse_args()
 
     import torch

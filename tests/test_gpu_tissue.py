@@ -355,13 +355,14 @@ def test_oracle_live_parity_random_config(ns):
     assert _rel(s.potential, o.potential) < 1e-9
 
 
-def test_cfg0_reference_cg_recurrences(golden, ns):
-    """cg_variant=0 runs the reference's recurrences verbatim (q = A p)."""
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_cfg0_all_cg_variants(golden, ns, variant):
+    """0: the reference's recurrences verbatim; 1: q by recurrence; 2: pipelined."""
     from paper_2308_01651_b200 import configs
     from paper_2308_01651_b200.simulation import TissueSolver
 
     g = golden("tissue_cfg0")
-    s = TissueSolver(configs.config0(ns), cg_variant=0)
+    s = TissueSolver(configs.config0(ns), cg_variant=variant)
     probes = g["probes"]
     pu = np.empty((800, probes.size))
     for k in range(800):
@@ -382,3 +383,22 @@ def test_single_block_and_multi_block_grids_agree(ns):
         runs.append((s.iterations_log(), s.potential))
     assert np.abs(runs[0][0] - runs[1][0]).max() <= 1
     assert _rel(runs[0][1], runs[1][1]) < 1e-10
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+def test_ttp06_slab_cg_variants(golden, ns, variant):
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    g = golden("tissue_ttp_h05")
+    s = TissueSolver(configs.config2(ns, h=0.5e-3), cg_variant=variant)
+    probes = g["probes"]
+    pu = np.empty((2000, probes.size))
+    for k in range(2000):
+        s.enqueue_step()
+        if (k + 1) % 100 == 0:
+            s.sync()
+    s.sync()
+    its = s.iterations_log()
+    assert np.abs(its - g["iters"]).max() <= 1
+    assert _rel(s.potential, g["final_u"]) < 1e-8
