@@ -167,6 +167,8 @@ def run_ours(args):
     ns = configs.this_package()
     cfg = configs.config2(ns)
     n = cfg.mesh.nodes.shape[0]
+    if world > 1:
+        return run_distributed(args, cfg, n, rank, world, local, dist)
     solver = TissueSolver(cfg)
     init_payload = solver.checkpoint_payload()   # host copy of the initial state
     for _ in range(args.warmup):
@@ -269,6 +271,49 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_distributed(args, cfg, n, rank, world, local, dist):
+    """N > 1: config 2 split over the ranks (z-slabs, NCCL halo + all-reduce),
+    strong scaling (total work fixed)."""
+    import torch
+
+    from paper_2308_01651_b200.distributed import DistributedTissueSolver
+
+    solver = DistributedTissueSolver(cfg)
+    for _ in range(args.warmup):
+        solver.step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(args.steps):
+            solver.step()
+        end.record()
+        dist.barrier()
+        torch.cuda.synchronize()
+    t = torch.tensor([start.elapsed_time(end)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    its = np.array(solver.iters[-args.steps:])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2 TTP06 slab 442,401 nodes, BDF2, dt=2e-5 s",
+                       "parallelism": f"z-slab domain decomposition x{world}, NCCL halo + "
+                                      "all-reduce, host-driven pipelined PCG",
+                       "cg_iters_per_step": [int(its.min()), float(its.mean()),
+                                             int(its.max())]},
+            "clocks": clocks.summary(),
+            "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def main():

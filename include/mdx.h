@@ -172,10 +172,20 @@ typedef struct mdx_cg_args {
   int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2);
                             2: pipelined PCG (1 reduction/iter) */
   int32_t _pad1;
+  /* distributed phases (mdx_pcg_phase): rows [row_begin, row_end) are the
+     rank-owned local rows; 0/0 = all rows */
+  int64_t row_begin, row_end;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */
 int mdx_pcg_solve(const mdx_cg_args* args, int tissue, int blocks_hint, void* stream);
+/* One phase of the distributed (multi-GPU) pipelined PCG: phase 0 init,
+ * 1 w0 = A u0, 2 sweep with host-supplied alpha/beta, 3 x = 0, 4 activation.
+ * mbuf selects the m buffer read (the other one is written). When sums_out
+ * is given, the phase's 4 partial sums are reduced (fixed order) into it.
+ * Rows [row_begin, row_end) of the local (owned + ghost) numbering. */
+int mdx_pcg_phase(const mdx_cg_args* args, int phase, int tissue, double alpha, double beta,
+                  int first, int mbuf, double* sums_out, void* stream);
 /* y = A x with the same row arithmetic (csr_matvec, linalg.py:17-23) */
 int mdx_spmv(const mdx_cg_args* args, const double* x, double* y, void* stream);
 

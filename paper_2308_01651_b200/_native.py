@@ -67,6 +67,7 @@ class CgArgs(C.Structure):
         ("partials_capacity", _i32), ("partials", _p), ("barrier", _p),
         ("iters_out", _p), ("relres_out", _p), ("status", _p),
         ("fail_step", _p), ("variant", _i32), ("_pad1", _i32),
+        ("row_begin", _i64), ("row_end", _i64),
     ]
 
 
@@ -105,6 +106,8 @@ _SIGNATURES = {
                          C.c_int),
     "mdx_tissue_prep": ([C.POINTER(TissueIonicArgs), _p], C.c_int),
     "mdx_pcg_solve": ([C.POINTER(CgArgs), C.c_int, C.c_int, _p], C.c_int),
+    "mdx_pcg_phase": ([C.POINTER(CgArgs), C.c_int, C.c_int, _d, _d, C.c_int, C.c_int, _p,
+                       _p], C.c_int),
     "mdx_spmv": ([C.POINTER(CgArgs), _p, _p, _p], C.c_int),
     "mdx_assemble_local": ([C.POINTER(AssemblyArgs), _p], C.c_int),
     "mdx_scatter_csr": ([_i64, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],

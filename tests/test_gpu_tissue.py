@@ -402,3 +402,33 @@ def test_ttp06_slab_cg_variants(golden, ns, variant):
     its = s.iterations_log()
     assert np.abs(its - g["iters"]).max() <= 1
     assert _rel(s.potential, g["final_u"]) < 1e-8
+
+
+def test_distributed_solver_single_rank_on_gpu(golden, ns):
+    """DistributedTissueSolver (phase kernels + NCCL plumbing) with one rank
+    reproduces the reference config-0 run (multi-rank host logic: gloo tests)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.distributed import DistributedTissueSolver
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        g = golden("tissue_cfg0")
+        s = DistributedTissueSolver(configs.config0(ns))
+        for _ in range(300):
+            s.step()
+        its = np.array(s.iters)
+        assert np.abs(its - g["iters"][:300]).max() <= 1
+        u = s.gather_potential()
+        assert _rel(u, g["snap_300"]) < 1e-9
+    finally:
+        dist.destroy_process_group()
