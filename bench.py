@@ -246,7 +246,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config2 TTP06 slab 20x7x3 mm h=0.1 mm (442,401 nodes), "
                                "BDF2, dt=2e-5 s, steps from rest (propagation phase)",
-                   "operator": "stencil27 class tables" if solver.op.kind == 1 else "csr",
+                   "operator": {1: "stencil27 class tables", 2: "csr", 3: "sell32"}[solver.op.kind],
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "state ring 255 MB > L2; no flush",
                    "cg_iters_per_step": [int(its.min()), float(its.mean()), int(its.max())]},

@@ -37,6 +37,9 @@ extern "C" {
 
 #define MDX_OP_STENCIL27 1 /* structured hex slab, node-class tables */
 #define MDX_OP_CSR 2       /* assembled CSR, int64 indptr / int32 indices */
+#define MDX_OP_SELL 3      /* SELL-32: rows in chunks of 32, entries column-major per chunk;
+                              indptr = chunk offsets (nchunks+1), indices = padded columns,
+                              padding entries have value 0 and column = the row itself */
 
 #define MDX_MAX_LIFT 8 /* volumes in the ICI lift (simulation.py:342-352) */
 
@@ -115,7 +118,7 @@ int mdx_tissue_prep(const mdx_tissue_ionic_args* args, void* stream);
 /*   finiteness check (:473-476) and _update_activation (:485-494).        */
 /* --------------------------------------------------------------------- */
 typedef struct mdx_operator {
-  int32_t kind;          /* MDX_OP_STENCIL27 or MDX_OP_CSR */
+  int32_t kind;          /* MDX_OP_STENCIL27, MDX_OP_CSR or MDX_OP_SELL */
   int32_t ncls;          /* stencil: number of node classes */
   int64_t n;             /* rows = nodes */
   int32_t nx1, ny1, nz1; /* stencil: nodes per axis (x fastest) */

@@ -24,6 +24,7 @@ MODEL_BUENO_OROVIO = 1
 MODEL_TTP06 = 2
 OP_STENCIL27 = 1
 OP_CSR = 2
+OP_SELL = 3
 MAX_LIFT = 8
 
 STATUS_DIVERGED = 1

@@ -135,10 +135,12 @@ class StencilOperator:
 
 
 class CsrOperator:
+    """Reference pattern, device-assembled values; SELL-32 layout by default."""
+
     kind = N.OP_CSR
 
     def __init__(self, dm, space, K_local, M_local, include_k, include_m,
-                 lift_includes, inactive, rest, thr, dt, orders):
+                 lift_includes, inactive, rest, thr, dt, orders, sell=True):
         torch = _torch()
         indptr, indices = space.pattern()
         self.n = dm.n
@@ -174,10 +176,52 @@ class CsrOperator:
                 raise ValueError("system matrix has non-positive diagonal")
             self.a_tables[order] = A
             self.dinv[order] = 1.0 / diag
+        if sell:
+            self._to_sell(indptr, indices)
+
+    def _to_sell(self, indptr, indices):
+        """Re-layout every value array as SELL-32 (coalesced warp loads).
+
+        Row order and the ascending-column order inside a row are kept, so
+        the row sums round exactly as on CSR; padding entries are (0, row).
+        """
+        torch = _torch()
+        n = self.n
+        lens = np.diff(indptr)
+        nch = (n + 31) // 32
+        padded = np.zeros(nch * 32, dtype=np.int64)
+        padded[:n] = lens
+        width = padded.reshape(nch, 32).max(axis=1)
+        cptr = np.zeros(nch + 1, dtype=np.int64)
+        np.cumsum(32 * width, out=cptr[1:])
+        rows = np.repeat(np.arange(n), lens)
+        j = np.arange(indices.size) - indptr[rows]
+        pos = cptr[rows // 32] + j * 32 + (rows % 32)
+        total = int(cptr[-1])
+        # column of every SELL slot: its own row for padding, then the real ones
+        within = np.arange(total) - np.repeat(cptr[:-1], 32 * width)
+        slot_row = (np.repeat(np.arange(nch), 32 * width) * 32 + within % 32)
+        cols = np.minimum(slot_row, n - 1).astype(np.int32)
+        cols[pos] = indices
+        dpos = torch.from_numpy(pos).cuda()
+
+        def relayout(vals):
+            out = torch.zeros(total, dtype=torch.float64, device="cuda")
+            out[dpos] = vals
+            return out
+
+        self.a_tables = {k: relayout(v) for k, v in self.a_tables.items()}
+        m_new = relayout(self.d_m)
+        self.d_lift = [m_new if v is self.d_m else relayout(v) for v in self.d_lift]
+        self.d_m = m_new
+        self.indptr = torch.from_numpy(cptr).cuda()
+        self.indices = torch.from_numpy(cols).cuda()
+        self.kind = N.OP_SELL
+        self.sell_slots = total
 
     def operator(self):
         op = N.Operator()
-        op.kind = N.OP_CSR
+        op.kind = self.kind
         op.n = self.n
         op.indptr = N.ptr(self.indptr)
         op.indices = N.ptr(self.indices)

@@ -385,7 +385,7 @@ class TissueSolver:
                 if operator == "stencil":
                     raise
         if self.op is None:
-            self.op = CsrOperator(dm, self.space, *args)
+            self.op = CsrOperator(dm, self.space, *args, sell=(operator != "csr"))
         del K_local, M_local, dm
 
         # device state

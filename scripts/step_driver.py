@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--operator", default="auto")
     ap.add_argument("--blocks", type=int, default=0)
     ap.add_argument("--variant", type=int, default=2)
+    ap.add_argument("--nodes", type=float, default=1e6, help="config 4 target size")
     args = ap.parse_args()
 
     import torch
@@ -32,10 +33,20 @@ def main():
 
     ns = configs.this_package()
     kw = {} if args.h is None else {"h": args.h}
-    cfg = {"0": configs.config0, "2": configs.config2, "3": configs.config3}[args.config](
-        ns, **kw)
+    if args.config == "4":
+        from paper_2308_01651_b200 import ventricle
+
+        t0 = time.perf_counter()
+        cfg = ventricle.config4(ns, *ventricle.size_for_nodes(args.nodes))
+        print(f"config 4 mesh: {cfg.mesh.nodes.shape[0]} nodes, "
+              f"{cfg.mesh.elements.shape[0]} tets, {time.perf_counter() - t0:.1f} s")
+    else:
+        cfg = {"0": configs.config0, "2": configs.config2, "3": configs.config3}[args.config](
+            ns, **kw)
+    t0 = time.perf_counter()
     s = TissueSolver(cfg, operator=args.operator, blocks_hint=args.blocks,
                      cg_variant=args.variant)
+    print(f"setup {time.perf_counter() - t0:.1f} s")
     for _ in range(args.warmup):
         s.enqueue_step()
     s.sync()

@@ -215,8 +215,14 @@ def tissue(name, build, steps, snap_every=None, payload_at=(), subsample=None):
     from monodomain.simulation import TissueSolver
 
     cfg = build(configs, ns)
-    probes = [ns.nearest_node(cfg.mesh, p) for p in configs.corner_probes()]
-    probes.append(ns.nearest_node(cfg.mesh, (10e-3, 3.5e-3, 1.5e-3)))
+    if cfg.mesh.element_kind.value == "Tet4" and cfg.mesh.nodes[:, 2].min() < -1e-3:
+        # ventricle: apex, base ring points, mid-wall equator
+        pts = [(0, 0, -45e-3), (0, 0, -55e-3), (30e-3, 0, 0), (0, 30e-3, 0),
+               (-30e-3, 0, 0), (0, -30e-3, 0), (25e-3, 0, -20e-3), (0, 32e-3, -30e-3),
+               (-27e-3, 0, -10e-3)]
+    else:
+        pts = configs.corner_probes() + [(10e-3, 3.5e-3, 1.5e-3)]
+    probes = [ns.nearest_node(cfg.mesh, p) for p in pts]
     solver = TissueSolver(cfg)
     its, pr, umin, umax, snaps, payloads, wall = _drive(solver, steps, probes,
                                                         snap_every, payload_at)
@@ -306,6 +312,11 @@ JOBS = {
     "tissue_cfg3_h05": lambda: tissue("tissue_cfg3_h05",
                                       lambda c, ns: c.config3(ns, h=0.5e-3), 25000,
                                       snap_every=2500, payload_at=(15000,)),
+    "tissue_cfg4_small": lambda: tissue(
+        "tissue_cfg4_small",
+        lambda c, ns: __import__("paper_2308_01651_b200.ventricle", fromlist=["config4"])
+        .config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3), 1500,
+        snap_every=500),
     "tissue_cfg2_head": lambda: tissue("tissue_cfg2_head", lambda c, ns: c.config2(ns),
                                        40, snap_every=20, subsample=97),
 }

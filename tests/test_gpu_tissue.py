@@ -153,7 +153,9 @@ def test_stencil_operator_matches_csr(ns):
     for cfg in (configs.config0(ns), configs.config3(ns, h=0.5e-3)):
         st = TissueSolver(cfg, operator="stencil")
         cs = TissueSolver(cfg, operator="csr")
+        sl = TissueSolver(cfg, operator="sell")
         assert st.op.kind == N.OP_STENCIL27 and cs.op.kind == N.OP_CSR
+        assert sl.op.kind == N.OP_SELL
         x = torch.from_numpy(np.random.default_rng(5).standard_normal(st.n)).cuda()
         for order in st.op.a_tables:
             ys = []
@@ -182,6 +184,12 @@ def test_stencil_operator_matches_csr(ns):
         orc = O.OracleTissue(cfg)
         orc._system(1.5)
         np.testing.assert_array_equal(orc.A.matvec(x.cpu().numpy()), ys[1])  # CSR: bitwise
+        a = N.CgArgs()
+        a.op = sl.op.operator()
+        a.a_val = N.ptr(sl.op.a_tables[1.5 and 2])
+        y = torch.empty_like(x)
+        N.check(N.lib().mdx_spmv(N.C.byref(a), N.ptr(x), N.ptr(y), N.stream_handle()))
+        np.testing.assert_array_equal(orc.A.matvec(x.cpu().numpy()), y.cpu().numpy())
 
 
 # ---------------------------------------------------------------------------
@@ -432,3 +440,17 @@ def test_distributed_solver_single_rank_on_gpu(golden, ns):
         assert _rel(u, g["snap_300"]) < 1e-9
     finally:
         dist.destroy_process_group()
+
+
+def test_cfg4_ventricle_small(golden, ns):
+    """Config-4 geometry (prolate-spheroid P1 tets, helix fibers, endo/mid/epi
+    volumes with duplicated interface states) on a reduced grid, CSR path."""
+    from paper_2308_01651_b200.simulation import TissueSolver
+    from paper_2308_01651_b200.ventricle import config4
+
+    g = golden("tissue_cfg4_small")
+    cfg = config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3)
+    s, pu = _run_against(g, cfg, 1500)
+    assert s.op.kind == 3                                   # SELL-32 (CSR pattern)
+    _check(s, pu, g, 2e-5, 1500)
+    assert _rel(s.potential, g["final_u"]) < 1e-8

@@ -180,3 +180,13 @@ def test_oracle_tissue_ttp_h05(golden, ns):
     assert np.array_equal(np.array(orc.iters), g["iters"])
     np.testing.assert_allclose(orc.potential, g["final_u"], rtol=0, atol=1e-12)
     np.testing.assert_array_equal(orc.activation_map, g["activation"])
+
+
+def test_oracle_cfg4_ventricle_small(golden, ns):
+    from paper_2308_01651_b200.ventricle import config4
+
+    g = golden("tissue_cfg4_small")
+    orc = O.OracleTissue(config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3))
+    for _ in range(300):
+        orc.step()
+    assert np.array_equal(np.array(orc.iters), g["iters"][:300])
