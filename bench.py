@@ -102,6 +102,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def traffic_of(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json, written by scripts/summarize_ncu.py), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        for k, v in d.items():
+            if kernel in k:
+                return v
+    return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -239,6 +251,22 @@ def run_ours(args):
     pcg_share = float(solve_ms.sum() / (ionic_ms.sum() + solve_ms.sum()))
     ionic_avg = float(ionic_ms.mean()) * 1e-3
     achieved = ionic_bytes / ionic_avg / 1e9
+    # algorithmic bytes of one persistent PCG launch (pipelined recurrences):
+    # RHS + r0/z0 (read combo, I, x, 4-B meta; write r, z) 44 B, w0/m0 24 B,
+    # activation ~41 B, and per CG iteration 116 B (read z s p x r w m + meta,
+    # write z s p x r w m') -- the stencil's neighbour reads counted once
+    pcg_bytes = n * (44 + 24 + 41 + 116 * its.astype(np.float64))
+    pcg_achieved = float((pcg_bytes / (solve_ms * 1e-3)).mean() / 1e9)
+    dominant_pcg = pcg_share > 0.5
+    roof_ionic = {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2>",
+                  "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
+                  "unit": "GB/s", "frac": achieved / hbm,
+                  "bytes_per_launch": ionic_bytes, "traffic": traffic_of("tissue_ionic")}
+    roof_pcg = {"bound": "hbm", "kernel": "pcg_kernel<STENCIL27,tissue> (L2-resident "
+                "vectors: HBM roofline is conservative)",
+                "achieved": pcg_achieved, "peak": hbm, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": pcg_achieved / hbm,
+                "bytes_per_launch": float(pcg_bytes.mean()), "traffic": traffic_of("pcg_kernel")}
     line = {
         "metric": METRIC, "value": n * args.steps * world / (ms * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -254,10 +282,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "kernels": {"ionic_ms": float(ionic_ms.mean()), "pcg_ms": float(solve_ms.mean()),
                     "pcg_share": pcg_share},
-        "roofline": {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2>",
-                     "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / hbm,
-                     "bytes_per_launch": ionic_bytes, "traffic": None},
+        "roofline": roof_pcg if dominant_pcg else roof_ionic,
+        "roofline_other": roof_ionic if dominant_pcg else roof_pcg,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": len(init_payload) / e2e_steps,
                 "d2h_bytes_per_step": 8 * (2 + len(probes))},

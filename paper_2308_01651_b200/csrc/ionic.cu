@@ -162,24 +162,29 @@ tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
     }
     const double u_ext = combine<ORDER>(uh, b.e);
 
-    double we[M::NV], wb[M::NV], wo[M::NV];
-#pragma unroll
-    for (int v = 0; v < M::NV; ++v) {
+    const int nslot = (a.head + 1) % S;
+    auto hist = [&](int v, const double* wts) {
       double wh[ORDER];
 #pragma unroll
       for (int k = 0; k < ORDER; ++k) {
         const int slot = (a.head - k + 3 * S) % S;
         wh[k] = a.w_ring[((int64_t)slot * M::NV + v) * a.ldw + i];
       }
-      wb[v] = combine<ORDER>(wh, b.h);
-      we[v] = M::NEEDS_WEXT ? combine<ORDER>(wh, b.e) : 0.0;
-    }
+      return combine<ORDER>(wh, wts);
+    };
+    auto store = [&](int v, double x) {
+      a.w_ring[((int64_t)nslot * M::NV + v) * a.ldw + i] = x;
+    };
     double I;
-    M::advance(u_ext, we, wb, b.alpha, a.dt, P, wo, I, local_clamp);
-    const int nslot = (a.head + 1) % S;
+    double we[M::NV], wb[M::NV], wo[M::NV];
 #pragma unroll
-    for (int v = 0; v < M::NV; ++v)
-      a.w_ring[((int64_t)nslot * M::NV + v) * a.ldw + i] = wo[v];
+    for (int v = 0; v < M::NV; ++v) {
+      wb[v] = hist(v, b.h);
+      we[v] = M::NEEDS_WEXT ? hist(v, b.e) : 0.0;
+    }
+    M::advance(u_ext, we, wb, b.alpha, a.dt, P, wo, I, local_clamp);
+#pragma unroll
+    for (int v = 0; v < M::NV; ++v) store(v, wo[v]);
     a.i_out[node] = I;
 
     if (a.prep) {

@@ -47,11 +47,24 @@ def stalls(d):
     return sorted(st, reverse=True)[:6]
 
 
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
 def main():
+    import json
+    from pathlib import Path
+
     out, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     lines = ["# ncu summary", ""]
+    traffic = {}
     for rep in reps:
         d, name = raw(rep)
+        try:
+            tb = sum(float(d[k][0]) * UNIT[d[k][1]] for k in
+                     ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            traffic[name.split("(")[0]] = tb
+        except (KeyError, ValueError):
+            pass
         lines += [f"## `{name[:110]}`", "", f"report: `{rep}`", "",
                   "| metric | value | unit |", "|---|---|---|"]
         for key, label in METRICS:
@@ -78,6 +91,7 @@ def main():
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"| `{k[:80]}` | {cnt[k]} | {v:.1f} | {v / all_t:.1%} |")
     open(out, "w").write("\n".join(lines) + "\n")
+    (Path(out).parent / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print("\n".join(lines))
 
 
