@@ -264,6 +264,10 @@ typedef struct mdx_pace_args {
 int mdx_pace_cells(int model, const mdx_pace_args* args, const double* P, int np,
                    void* stream);
 
+/* One run() output row (simulation.py:670-681): row = [min u, max u, u[probes]] */
+int mdx_record_row(const double* u, int64_t n, const int64_t* probes, int nprobes,
+                   double* row, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

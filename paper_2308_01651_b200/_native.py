@@ -119,6 +119,7 @@ _SIGNATURES = {
     "mdx_combine_system": ([_i64, _d, _p, _p, _p, _p], C.c_int),
     "mdx_pace_cells": ([C.c_int, C.POINTER(PaceArgs), _p, C.c_int, _p],
                        C.c_int),
+    "mdx_record_row": ([_p, _i64, _p, C.c_int, _p, _p], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -340,6 +340,38 @@ pace_cells(mdx_pace_args a, const typename M::Params P) {
   if (a.clamp_count && nclamp) atomicAdd(a.clamp_count, (unsigned long long)nclamp);
 }
 
+// One output row of run() (simulation.py:670-681): u_min, u_max, u[probes].
+__global__ void __launch_bounds__(1024)
+record_row(const double* __restrict__ u, int64_t n, const int64_t* __restrict__ probes,
+           int nprobes, double* __restrict__ row) {
+  __shared__ double smin[32], smax[32];
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = u[i];
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smin[threadIdx.x >> 5] = lo;
+    smax[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, smin[w]);
+      hi = fmax(hi, smax[w]);
+    }
+    row[0] = lo;
+    row[1] = hi;
+  }
+  for (int k = threadIdx.x; k < nprobes; k += blockDim.x) row[2 + k] = u[probes[k]];
+}
+
 template <class M>
 static typename M::Params load_params(const double* P, int np, int* err) {
   typename M::Params p;
@@ -501,6 +533,13 @@ int mdx_tissue_prep(const mdx_tissue_ionic_args* a, void* stream) {
     default: set_error("BDF order %d", a->order); return MDX_ERR_ARG;
   }
   return check_launch("mdx_tissue_prep");
+}
+
+int mdx_record_row(const double* u, int64_t n, const int64_t* probes, int nprobes,
+                   double* row, void* stream) {
+  if (n <= 0) return MDX_OK;
+  record_row<<<1, 1024, 0, (cudaStream_t)stream>>>(u, n, probes, nprobes, row);
+  return check_launch("mdx_record_row");
 }
 
 int mdx_pace_cells(int model, const mdx_pace_args* args, const double* P, int np,

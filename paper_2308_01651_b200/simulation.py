@@ -669,6 +669,21 @@ class TissueSolver:
         fr = self.frozen.cpu().numpy().astype(bool)
         return bool(fr[~self.inactive].all())
 
+    def record_row(self, probe_idx, dst):
+        """Asynchronously copy [u_min, u_max, u[probes]] of the current
+        potential into `dst` (a pinned host tensor row): one kernel and one
+        D2H copy, no synchronisation."""
+        import torch
+
+        k = 2 + (0 if probe_idx is None else probe_idx.numel())
+        if getattr(self, "_row_dev", None) is None or self._row_dev.numel() < k:
+            self._row_dev = torch.empty(k, dtype=torch.float64, device="cuda")
+        N.check(N.lib().mdx_record_row(
+            N.ptr(self.potential_device), self.n, N.ptr(probe_idx),
+            0 if probe_idx is None else probe_idx.numel(), N.ptr(self._row_dev),
+            N.stream_handle()), "mdx_record_row")
+        dst.copy_(self._row_dev[:k], non_blocking=True)
+
     def clamp_total(self):
         return int(self.clamps.item())
 
@@ -826,20 +841,18 @@ def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
         solver.restore(load_checkpoint(resume_from))
     n_steps = int(round(config.final_time / config.dt))
     out = getattr(config, "output", None) or OutputConfig()
-    rows, vtk_paths = [], []
+    vtk_paths = []
     probes = [nearest_node(config.mesh, p) for p in out.probe_points]
     probe_idx = torch.tensor(probes, dtype=torch.int64, device="cuda") if probes else None
+    n_rec = (n_steps - solver.step_index) // out.stride + 2
+    pinned = torch.empty((n_rec, 2 + len(probes)), dtype=torch.float64, pin_memory=True)
+    times = []
 
     def record():
         with solver.timer.section("Other"):
             if out.enable_csv or not out.enable_field_output:
-                u = solver.potential_device
-                mm = torch.aminmax(u)
-                vals = [mm.min.reshape(1), mm.max.reshape(1)]
-                if probe_idx is not None:
-                    vals.append(u[probe_idx])
-                row = torch.cat(vals).cpu().numpy()
-                rows.append((solver.time, *row.tolist()))
+                solver.record_row(probe_idx, pinned[len(times)])   # async D2H
+                times.append(solver.time)
             if out.enable_field_output:
                 path = f"{out.field_stem}_{solver.step_index:06d}.vtk"
                 write_vtk(path, config.mesh, {"transmembrane_potential": solver.potential})
@@ -851,11 +864,11 @@ def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
         solver.enqueue_step()
         k = solver.step_index
         if k % out.stride == 0 or k == n_steps:
-            solver.sync()
             record()
         if stop_when_fully_activated and solver.fully_activated():
             break
     solver.sync()
+    rows = [(t, *pinned[i].tolist()) for i, t in enumerate(times)]
     with solver.timer.section("Other"):
         csv_path = None
         if out.enable_csv:

@@ -454,3 +454,29 @@ def test_cfg4_ventricle_small(golden, ns):
     assert s.op.kind == 3                                   # SELL-32 (CSR pattern)
     _check(s, pu, g, 2e-5, 1500)
     assert _rel(s.potential, g["final_u"]) < 1e-8
+
+
+def test_run_loop_rows_csv_and_vtk(golden, ns, tmp_path):
+    """run() (simulation.py:651-716): output rows, CSV/VTK writers, report."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.outputs import OutputConfig
+    from paper_2308_01651_b200.simulation import ActivationConfig, run
+
+    g = golden("tissue_cfg0")
+    cfg = configs.config0(ns, final_time=100 * 5e-5)
+    pts = [tuple(ns_node) for ns_node in cfg.mesh.nodes[g["probes"]]]
+    cfg.output = OutputConfig(enable_csv=True, csv_path=str(tmp_path / "t.csv"), stride=10,
+                              probe_points=tuple(pts))
+    cfg.activation = ActivationConfig(enabled=True, path=str(tmp_path / "act.vtk"),
+                                      threshold=84.0 / 85.7)
+    rep = run(cfg)
+    assert rep.steps == 100
+    rows = np.array(rep.rows)
+    assert rows.shape == (11, 3 + len(pts))
+    np.testing.assert_allclose(rows[1:, 3:], g["probe_u"][9:100:10], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(rows[1:, 2], g["umax"][9:100:10], rtol=1e-9)
+    text = (tmp_path / "t.csv").read_text().splitlines()
+    assert text[0].startswith("t,u_min,u_max,probe_0") and len(text) == 12
+    assert (tmp_path / "act.vtk").read_text().startswith("# vtk DataFile Version 3.0")
+    assert rep.max_cg_iterations == int(g["iters"][:100].max()) or \
+        abs(rep.max_cg_iterations - int(g["iters"][:100].max())) <= 1
