@@ -348,7 +348,7 @@ class TissueSolver:
         w0 = {}
         for vol in by_desc:
             state, trace = vol.initial_cell_state(cfg.bdf_order)
-            w0[id(vol)] = np.broadcast_to(state.w, (vol.dofs.size, vol.num_vars))
+            w0[id(vol)] = np.asarray(state.w, dtype=np.float64)
             u0[vol.dofs] = state.u
             rest[vol.dofs] = vol.rest_u
             thr[vol.dofs] = vol.threshold
@@ -400,8 +400,7 @@ class TissueSolver:
             lw = _pad(vol.dofs.size)
             vol.ldw = lw
             vol.w_ring = torch.zeros((RING_SLOTS, vol.num_vars, lw), **f64)
-            vol.w_ring[0, :, :vol.dofs.size] = torch.from_numpy(
-                np.ascontiguousarray(w0[id(vol)].T)).cuda()
+            vol.w_ring[0, :, :vol.dofs.size] = torch.from_numpy(w0[id(vol)]).cuda()[:, None]
             vol.w_fill = 1
             vol.d_dofs = (None if (vol.dofs.size == n and vol.dofs[-1] == n - 1)
                           else torch.from_numpy(vol.dofs.astype(np.int32)).cuda())
@@ -774,8 +773,9 @@ class TissueSolver:
         self.u_fill = fill
         for vol, states in zip(self.volumes, vol_states):
             for k, w in enumerate(states):
+                # upload the reference's AoS block as is; transpose on the device
                 vol.w_ring[(-k) % RING_SLOTS, :, : vol.dofs.size] = \
-                    torch.from_numpy(np.ascontiguousarray(w.T)).cuda()
+                    torch.from_numpy(w).cuda().t()
             vol.w_fill = len(states)
         self.act_time.copy_(torch.from_numpy(act))
         self.best_slope.copy_(torch.from_numpy(best))
