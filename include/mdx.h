@@ -166,7 +166,7 @@ typedef struct mdx_cg_args {
   double tol;
   int32_t max_iter;
   int32_t partials_capacity; /* blocks the partials buffer can hold */
-  double* partials;      /* [partials_capacity][4] */
+  double* partials;      /* [2][partials_capacity][4] (double-buffered) */
   unsigned long long* barrier; /* grid-barrier counter, zero-initialised, reused */
   int32_t* iters_out;    /* iterations (reference convention: -max_iter) */
   double* relres_out;
@@ -174,7 +174,8 @@ typedef struct mdx_cg_args {
   int32_t* fail_step;    /* receives `step` when status is raised */
   int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2);
                             2: pipelined PCG (1 reduction/iter) */
-  int32_t _pad1;
+  int32_t dom_class1;    /* stencil: 1 + id of the dominant interior class whose
+                            coefficients are staged in constant memory (0 = none) */
   /* distributed phases (mdx_pcg_phase): rows [row_begin, row_end) are the
      rank-owned local rows; 0/0 = all rows */
   int64_t row_begin, row_end;

@@ -67,7 +67,7 @@ class CgArgs(C.Structure):
         ("t_next", _d), ("dt", _d), ("tol", _d), ("max_iter", _i32),
         ("partials_capacity", _i32), ("partials", _p), ("barrier", _p),
         ("iters_out", _p), ("relres_out", _p), ("status", _p),
-        ("fail_step", _p), ("variant", _i32), ("_pad1", _i32),
+        ("fail_step", _p), ("variant", _i32), ("dom_class1", _i32),
         ("row_begin", _i64), ("row_end", _i64),
     ]
 

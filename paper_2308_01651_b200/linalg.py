@@ -30,7 +30,7 @@ class CgWorkspace:
             props = torch.cuda.get_device_properties(0)
             max_blocks = props.multi_processor_count * 8
         self.capacity = int(max_blocks)
-        self.partials = torch.zeros(self.capacity * 4, dtype=torch.float64, device="cuda")
+        self.partials = torch.zeros(self.capacity * 8, dtype=torch.float64, device="cuda")
         self.barrier = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.p = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.q = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")

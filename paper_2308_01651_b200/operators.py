@@ -76,6 +76,10 @@ class StencilOperator:
         mask = ((i > 0) * 1 | (i < nx) * 2 | (j > 0) * 4 | (j < ny) * 8 | (k > 0) * 16
                 | (k < nz) * 32).astype(np.uint32)
         self.meta = torch.from_numpy(inverse.astype(np.uint32) | (mask << 16)).cuda()
+        # the most frequent class among nodes with all 26 neighbours (the
+        # solver stages its row in the constant bank); -1 when there is none
+        full = inverse[mask == 63]
+        self.dom_class = int(np.bincount(full).argmax()) if full.size else -1
         rep = torch.from_numpy(first.astype(np.int64)).cuda()
         bad = torch.zeros(2, dtype=torch.int64, device="cuda")
         N.check(N.lib().mdx_verify_classes(self.n, nblk, 3, N.ptr(key), N.ptr(self.cls),

@@ -28,6 +28,7 @@ rolls its step counter back to the failed step and raises the reference's
 exception (`SolverDivergence`, `NonFiniteSolution`).
 """
 
+import os
 import struct
 import time
 import zlib
@@ -507,6 +508,9 @@ class TissueSolver:
         a.max_iter = cfg.linear_solver.max_iterations
         self.ws.fill(a)
         a.variant = self.cg_variant
+        a.dom_class1 = getattr(op, "dom_class", -1) + 1
+        if os.environ.get("MDX_DOM_CLASS") == "0":      # ablation switch
+            a.dom_class1 = 0
         self._cg_args = a
         self._a_ptr = {k: N.ptr(v) for k, v in op.a_tables.items()}
         self._dinv_ptr = {k: N.ptr(v) for k, v in op.dinv.items()}
