@@ -80,7 +80,7 @@ __device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned int 
     const unsigned long long target = (old / nblocks + 1) * nblocks;
     unsigned long long cur;
     do {
-      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+      asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
     } while (cur < target);
     __threadfence();
   }
