@@ -13,4 +13,5 @@ while [ $# -gt 0 ]; do
     -o $B/variants/solver_$name.o -Xptxas -v 2>&1 | grep -A2 "pcg_kernelILi1ELb1ELi[0-9]ELb1" | grep -E "registers|spill" | head -2 | sed "s/^/[$name] /"
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $B/ionic.o \
     $B/assembly.o $B/variants/solver_$name.o -o $B/variants/libmdx_$name.so
+  rm -f $B/variants/solver_$name.o
 done

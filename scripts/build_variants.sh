@@ -13,4 +13,5 @@ while [ $# -gt 0 ]; do
     -o $B/variants/ionic_$name.o -Xptxas -v 2>&1 | grep -A2 "tissue_ionicINS_5TTP06ELi2" | grep -E "registers|spill" | sed "s/^/[$name] /"
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $B/variants/ionic_$name.o \
     $B/assembly.o $B/solver.o -o $B/variants/libmdx_$name.so
+  rm -f $B/variants/ionic_$name.o
 done

@@ -1,6 +1,8 @@
 """Per-block timeline of one persistent PCG launch (debug build with
--DMDX_PCG_TRACE): phase time = arrive(k) - release(k-1), wait = release -
-arrive, per reduction k.  Usage: MDX_LIB=<trace .so> python scripts/pcg_trace.py"""
+-DMDX_PCG_TRACE): per reduction k, phase = arrive(k) - release(k-1) and
+wait = release(k) - arrive(k); inside the wait: block sums + publish,
+arrival atomic, spin until the last arrival, partial loads.
+Usage: MDX_LIB=<trace .so> python scripts/pcg_trace.py [blocks] [variant]"""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -10,50 +12,51 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-def main():
-    import torch
+def stats(x):
+    return f"{np.min(x) / 1e3:6.2f} {np.median(x) / 1e3:6.2f} {np.max(x) / 1e3:6.2f}"
 
+
+def main():
     from paper_2308_01651_b200 import _native as N, configs
     from paper_2308_01651_b200.simulation import TissueSolver
 
     cfg = configs.config2(configs.this_package())
     blocks = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-    s = TissueSolver(cfg, blocks_hint=blocks, cg_variant=int(sys.argv[2]) if len(sys.argv) > 2 else 2)
+    variant = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    s = TissueSolver(cfg, blocks_hint=blocks, cg_variant=variant)
     for _ in range(6):
         s.enqueue_step()
     s.sync()
     lib = N.lib()
-    lib.mdx_debug_trace.argtypes = [C.c_void_p]
-    buf = np.zeros((512, 256, 2), dtype=np.uint64)
-    lib.mdx_debug_trace(buf.ctypes.data_as(C.c_void_p))
+
+    def grab(name, shape):
+        fn = getattr(lib, name)
+        fn.argtypes = [C.c_void_p]
+        buf = np.zeros(shape, dtype=np.uint64)
+        fn(buf.ctypes.data_as(C.c_void_p))
+        return buf
+
+    buf = grab("mdx_debug_trace", (512, 256, 2))
+    bx = grab("mdx_debug_trace_x", (512, 256, 2))
+    by = grab("mdx_debug_trace_y", (512, 256))
     its = s.iterations_log()[-1]
-    used = buf[:, :, 0].any(axis=1)
-    nb = int(used.sum())
+    nb = int(buf[:, :, 0].any(axis=1).sum())
     ne = int((buf[0, :, 0] > 0).sum())
     t = buf[:nb, :ne, :].astype(np.int64)
     t0 = t[:, 0, 0].min()
-    arrive = t[:, :, 0] - t0
-    release = t[:, :, 1] - t0
-    X = None
-    if hasattr(lib, "mdx_debug_trace_x"):
-        lib.mdx_debug_trace_x.argtypes = [C.c_void_p]
-        bx = np.zeros((512, 256, 2), dtype=np.uint64)
-        lib.mdx_debug_trace_x(bx.ctypes.data_as(C.c_void_p))
-        X = bx[:nb, :ne, :].astype(np.int64) - t0
+    arrive, release = t[:, :, 0] - t0, t[:, :, 1] - t0
+    pub, cnt = bx[:nb, :ne, 0].astype(np.int64) - t0, bx[:nb, :ne, 1].astype(np.int64) - t0
+    rel = by[:nb, :ne].astype(np.int64) - t0
     print(f"blocks {nb}, reductions {ne}, CG iterations {its}")
-    print(f"kernel span {release.max() / 1e3:.1f} us")
-    for k in range(min(ne, 12)):
-        ph = arrive[:, k] - (release[:, k - 1] if k else arrive[:, 0] * 0)
-        wait = release[:, k] - arrive[:, k]
-        if X is not None and k > 1 and k < ne:
-            fx = X[:, k, 0] - arrive[:, k]      # arrival -> neighbour flags seen
-            sx = X[:, k, 1] - X[:, k, 0]            # stencil
-            print(f"        flags-wait min/med/max {fx.min()/1e3:6.2f} {np.median(fx)/1e3:6.2f} "
-                  f"{fx.max()/1e3:6.2f} us | stencil {sx.min()/1e3:6.2f} {np.median(sx)/1e3:6.2f} "
-                  f"{sx.max()/1e3:6.2f} us")
-        print(f"red {k:2d}: phase min/med/max {ph.min()/1e3:6.2f} {np.median(ph)/1e3:6.2f} "
-              f"{ph.max()/1e3:6.2f} us | wait min/med/max {wait.min()/1e3:6.2f} "
-              f"{np.median(wait)/1e3:6.2f} {wait.max()/1e3:6.2f} us")
+    print(f"kernel span {release.max() / 1e3:.1f} us   (min/med/max in us)")
+    for k in range(1, min(ne, 12)):
+        ph = arrive[:, k] - release[:, k - 1]
+        last = int(np.argmax(arrive[:, k]))
+        print(f"red {k:2d}: phase {stats(ph)} | wait {stats(release[:, k] - arrive[:, k])} | "
+              f"blocksum {stats(pub[:, k] - arrive[:, k])} | atomic {stats(cnt[:, k] - pub[:, k])}"
+              f" | spin(last block) {(rel[last, k] - cnt[last, k]) / 1e3:5.2f} | "
+              f"last-arrival->release {stats(rel[:, k] - pub[:, k].max())} | "
+              f"loads {stats(release[:, k] - rel[:, k])}")
 
 
 if __name__ == "__main__":
