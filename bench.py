@@ -103,15 +103,25 @@ class ClockSampler:
 
 
 def traffic_of(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/ncu_traffic.json, written by scripts/summarize_ncu.py), or None."""
+    """ncu figures of one launch of `kernel` from the committed capture
+    (profiles/ncu_traffic.json, written by scripts/summarize_ncu.py):
+    {"dram_bytes", "fp64_flops", ...}, or None."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         d = json.loads(p.read_text())
         for k, v in d.items():
             if kernel in k:
-                return v
+                return v if isinstance(v, dict) else {"dram_bytes": v}
     return None
+
+
+def fp64_peak_tflops():
+    """FP64 FMA peak: profiles/fp64_peak.json (scripts/fp64_peak.cu run on the
+    box), else the nominal 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz."""
+    p = ROOT / "profiles" / "fp64_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["fp64_tflops"]), "measured"
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal"
 
 
 def dist_env():
@@ -240,30 +250,46 @@ def run_ours(args):
     e2e_value = n * e2e_steps * world / e2e_wall
 
     hbm, peak_kind = peaks()
-    order = 2
+    fp64_peak, fp64_kind = fp64_peak_tflops()
     nv = 18
-    # algorithmic bytes of the fused TTP06 update (BDF2, single volume):
-    # read u_n,u_{n-1}, W_n,W_{n-1}; write W_{n+1}, I, combo, x0
-    ionic_bytes = n * 8 * (order + order * nv + nv + 3)
+    steps_k = its.astype(np.float64)
+    # SURVEY.md 8(d) algorithmic bytes per node-step (fp64, BDF2, fused design):
+    #   ionic update 8*(3nv+3) = 456 (read u_n, u_n-1, W_n, W_n-1; write W_n+1, c)
+    #   PCG launch: RHS 16 + CG setup 56 + activation 34 + 104 per CG iteration
+    #   whole step 562 + 104 k, k = this step's CG iterations
+    ionic_bytes = n * 8 * (3 * nv + 3)
+    pcg_bytes = n * (16 + 56 + 34 + 104 * steps_k)
+    step_bytes = n * (562 + 104 * steps_k)
     pcg_share = float(solve_ms.sum() / (ionic_ms.sum() + solve_ms.sum()))
     ionic_avg = float(ionic_ms.mean()) * 1e-3
     achieved = ionic_bytes / ionic_avg / 1e9
-    # algorithmic bytes of one persistent PCG launch (pipelined recurrences):
-    # RHS + r0/z0 (read combo, I, x, 4-B meta; write r, z) 44 B, w0/m0 24 B,
-    # activation ~41 B, and per CG iteration 116 B (read z s p x r w m + meta,
-    # write z s p x r w m') -- the stencil's neighbour reads counted once
-    pcg_bytes = n * (44 + 24 + 41 + 116 * its.astype(np.float64))
-    pcg_achieved = float((pcg_bytes / (solve_ms * 1e-3)).mean() / 1e9)
+    pcg_achieved = float(pcg_bytes.sum() / (solve_ms.sum() * 1e-3) / 1e9)
+    step_achieved = float(step_bytes.sum() / (ms * 1e-3) / 1e9)
     dominant_pcg = pcg_share > 0.5
+    t_ionic = traffic_of("tissue_ionic")
     roof_ionic = {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2>",
                   "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
                   "unit": "GB/s", "frac": achieved / hbm,
-                  "bytes_per_launch": ionic_bytes, "traffic": traffic_of("tissue_ionic")}
-    roof_pcg = {"bound": "hbm", "kernel": "pcg_kernel<STENCIL27,tissue> (L2-resident "
-                "vectors: HBM roofline is conservative)",
+                  "bytes_per_launch": ionic_bytes,
+                  "traffic": t_ionic.get("dram_bytes") if t_ionic else None}
+    if t_ionic and t_ionic.get("fp64_flops"):
+        # FP64 flops per cell from the ncu SASS counts of one launch (per-cell
+        # constant up to branch divergence), scaled to this launch's n
+        flops = t_ionic["fp64_flops"] / t_ionic.get("n", n) * n
+        roof_ionic["fp64"] = {"achieved": flops / ionic_avg / 1e12, "peak": fp64_peak,
+                              "peak_kind": fp64_kind, "unit": "TFLOP/s",
+                              "frac": flops / ionic_avg / 1e12 / fp64_peak,
+                              "flops_per_launch": flops}
+    t_pcg = traffic_of("pcg_resident_kernel") or traffic_of("pcg_kernel")
+    roof_pcg = {"bound": "hbm", "kernel": "pcg_resident_kernel<tissue,3> (vectors in SMEM: "
+                "HBM roofline of the unfused algorithm's bytes)",
                 "achieved": pcg_achieved, "peak": hbm, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": pcg_achieved / hbm,
-                "bytes_per_launch": float(pcg_bytes.mean()), "traffic": traffic_of("pcg_kernel")}
+                "bytes_per_launch": float(pcg_bytes.mean()),
+                "traffic": t_pcg.get("dram_bytes") if t_pcg else None}
+    roof_step = {"bound": "hbm", "achieved": step_achieved, "peak": hbm, "unit": "GB/s",
+                 "frac": step_achieved / hbm, "bytes_per_step": float(step_bytes.mean()),
+                 "formula": "n*(562 + 104*k) per step (SURVEY.md 8(d))"}
     line = {
         "metric": METRIC, "value": n * args.steps * world / (ms * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -281,6 +307,7 @@ def run_ours(args):
                     "pcg_share": pcg_share},
         "roofline": roof_pcg if dominant_pcg else roof_ionic,
         "roofline_other": roof_ionic if dominant_pcg else roof_pcg,
+        "roofline_step": roof_step,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": len(init_payload) / e2e_steps,
                 "d2h_bytes_per_step": 8 * (2 + len(probes))},

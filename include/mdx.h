@@ -265,9 +265,12 @@ typedef struct mdx_pace_args {
 int mdx_pace_cells(int model, const mdx_pace_args* args, const double* P, int np,
                    void* stream);
 
-/* One run() output row (simulation.py:670-681): row = [min u, max u, u[probes]] */
+/* One run() output row (simulation.py:670-681): row = [min u, max u, u[probes]].
+   scratch: MDX_ROW_SCRATCH doubles, zero-initialised once, reused (per-block
+   partials + a completion counter); one call at a time per scratch buffer. */
+#define MDX_ROW_SCRATCH 1024
 int mdx_record_row(const double* u, int64_t n, const int64_t* probes, int nprobes,
-                   double* row, void* stream);
+                   double* row, double* scratch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ MODEL_TTP06 = 2
 OP_STENCIL27 = 1
 OP_CSR = 2
 OP_SELL = 3
+ROW_SCRATCH = 1024        # MDX_ROW_SCRATCH
 MAX_LIFT = 8
 
 STATUS_DIVERGED = 1
@@ -119,7 +120,7 @@ _SIGNATURES = {
     "mdx_combine_system": ([_i64, _d, _p, _p, _p, _p], C.c_int),
     "mdx_pace_cells": ([C.c_int, C.POINTER(PaceArgs), _p, C.c_int, _p],
                        C.c_int),
-    "mdx_record_row": ([_p, _i64, _p, C.c_int, _p, _p], C.c_int),
+    "mdx_record_row": ([_p, _i64, _p, C.c_int, _p, _p, _p], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

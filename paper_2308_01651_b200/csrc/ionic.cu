@@ -9,6 +9,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "ionic_models.cuh"
 
@@ -346,12 +348,18 @@ pace_cells(mdx_pace_args a, const typename M::Params P) {
 }
 
 // One output row of run() (simulation.py:670-681): u_min, u_max, u[probes].
-__global__ void __launch_bounds__(1024)
+// Multi-block min/max: every block writes its partial, the last block to
+// finish (completion counter) combines them in block order and resets the
+// counter; block 0 gathers the probes.
+constexpr int ROW_MAX_BLOCKS = (MDX_ROW_SCRATCH - 8) / 2;
+__global__ void __launch_bounds__(256)
 record_row(const double* __restrict__ u, int64_t n, const int64_t* __restrict__ probes,
-           int nprobes, double* __restrict__ row) {
-  __shared__ double smin[32], smax[32];
+           int nprobes, double* __restrict__ row, double* scratch) {
+  __shared__ double smin[8], smax[8];
+  __shared__ bool last;
   double lo = INFINITY, hi = -INFINITY;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
     const double v = u[i];
     lo = fmin(lo, v);
     hi = fmax(hi, v);
@@ -366,15 +374,32 @@ record_row(const double* __restrict__ u, int64_t n, const int64_t* __restrict__ 
     smax[threadIdx.x >> 5] = hi;
   }
   __syncthreads();
+  unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + 2 * ROW_MAX_BLOCKS);
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
       lo = fmin(lo, smin[w]);
       hi = fmax(hi, smax[w]);
     }
+    scratch[2 * blockIdx.x] = lo;
+    scratch[2 * blockIdx.x + 1] = hi;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < nprobes; k += blockDim.x) row[2 + k] = u[probes[k]];
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    lo = INFINITY;
+    hi = -INFINITY;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      lo = fmin(lo, __ldcg(scratch + 2 * b));
+      hi = fmax(hi, __ldcg(scratch + 2 * b + 1));
+    }
     row[0] = lo;
     row[1] = hi;
+    *counter = 0u;
   }
-  for (int k = threadIdx.x; k < nprobes; k += blockDim.x) row[2 + k] = u[probes[k]];
 }
 
 template <class M>
@@ -542,9 +567,13 @@ int mdx_tissue_prep(const mdx_tissue_ionic_args* a, void* stream) {
 }
 
 int mdx_record_row(const double* u, int64_t n, const int64_t* probes, int nprobes,
-                   double* row, void* stream) {
+                   double* row, double* scratch, void* stream) {
   if (n <= 0) return MDX_OK;
-  record_row<<<1, 1024, 0, (cudaStream_t)stream>>>(u, n, probes, nprobes, row);
+  int64_t g = (n + 256 * 8 - 1) / (256 * 8);
+  const int64_t cap = std::min<int64_t>(ROW_MAX_BLOCKS, 2 * (int64_t)num_sms());
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  record_row<<<(int)g, 256, 0, (cudaStream_t)stream>>>(u, n, probes, nprobes, row, scratch);
   return check_launch("mdx_record_row");
 }
 

@@ -681,10 +681,12 @@ class TissueSolver:
         k = 2 + (0 if probe_idx is None else probe_idx.numel())
         if getattr(self, "_row_dev", None) is None or self._row_dev.numel() < k:
             self._row_dev = torch.empty(k, dtype=torch.float64, device="cuda")
+        if getattr(self, "_row_scratch", None) is None:
+            self._row_scratch = torch.zeros(N.ROW_SCRATCH, dtype=torch.float64, device="cuda")
         N.check(N.lib().mdx_record_row(
             N.ptr(self.potential_device), self.n, N.ptr(probe_idx),
             0 if probe_idx is None else probe_idx.numel(), N.ptr(self._row_dev),
-            N.stream_handle()), "mdx_record_row")
+            N.ptr(self._row_scratch), N.stream_handle()), "mdx_record_row")
         dst.copy_(self._row_dev[:k], non_blocking=True)
 
     def clamp_total(self):
@@ -739,11 +741,15 @@ class TissueSolver:
         step_index, t = struct.unpack_from("<Qd", payload, off)
         off += struct.calcsize("<Qd")
 
+        # parse the layout on the host (header fields only), upload the whole
+        # payload in one H2D copy and cut the arrays out on the device
+        segs = []
+
         def take(count, dtype=np.float64):
             nonlocal off
-            arr = np.frombuffer(payload, dtype=dtype, count=count, offset=off).copy()
+            segs.append((off, count, np.dtype(dtype)))
             off += count * np.dtype(dtype).itemsize
-            return arr
+            return len(segs) - 1
 
         (fill,) = struct.unpack_from("<I", payload, off)
         off += 4
@@ -760,7 +766,7 @@ class TissueSolver:
         for vol in self.volumes:
             (ll,) = struct.unpack_from("<I", payload, off)
             off += 4
-            label = payload[off: off + ll].decode("utf-8")
+            label = bytes(payload[off: off + ll]).decode("utf-8")
             off += ll
             if label != vol.config.label:
                 raise CorruptFile(f"checkpoint volume {label!r} does not match "
@@ -769,21 +775,38 @@ class TissueSolver:
             off += struct.calcsize("<IQI")
             if nv != vol.num_vars or nd != vol.dofs.size:
                 raise DofCountMismatch(f"checkpoint volume {label!r} shape mismatch")
-            vol_states.append([take(nd * nv).reshape(nd, nv) for _ in range(wf)])
+            vol_states.append([(take(nd * nv), nd, nv) for _ in range(wf)])
+        if off > len(payload):
+            raise CorruptFile("checkpoint payload truncated")
+        import warnings
+
+        with warnings.catch_warnings():          # read-only bytes: never written
+            warnings.simplefilter("ignore", UserWarning)
+            raw = torch.frombuffer(payload, dtype=torch.uint8, count=off)
+        dev = raw.to("cuda")
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8}
+
+        def seg(k):
+            o, count, dt = segs[k]
+            nb = count * dt.itemsize
+            b = dev[o: o + nb]
+            if o % dt.itemsize:
+                b = b.clone()                     # re-align on the device
+            return b.view(tdt[dt])
+
         # newest first -> slots head, head-1, ...
         self.head = 0
         for k, u in enumerate(us):
-            self.u_ring[(-k) % RING_SLOTS, :n] = torch.from_numpy(u).cuda()
+            self.u_ring[(-k) % RING_SLOTS, :n] = seg(u)
         self.u_fill = fill
         for vol, states in zip(self.volumes, vol_states):
-            for k, w in enumerate(states):
-                # upload the reference's AoS block as is; transpose on the device
-                vol.w_ring[(-k) % RING_SLOTS, :, : vol.dofs.size] = \
-                    torch.from_numpy(w).cuda().t()
+            for k, (w, nd, nv) in enumerate(states):
+                # the reference's AoS block, transposed to SoA on the device
+                vol.w_ring[(-k) % RING_SLOTS, :, :nd] = seg(w).view(nd, nv).t()
             vol.w_fill = len(states)
-        self.act_time.copy_(torch.from_numpy(act))
-        self.best_slope.copy_(torch.from_numpy(best))
-        self.frozen.copy_(torch.from_numpy(frozen))
+        self.act_time.copy_(seg(act))
+        self.best_slope.copy_(seg(best))
+        self.frozen.copy_(seg(frozen).view(self.frozen.dtype))
         self.step_index, self.time = int(step_index), float(t)
         self._log_base = self.step_index
         self.ws.status.zero_()

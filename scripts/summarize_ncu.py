@@ -15,6 +15,8 @@ METRICS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe % active"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst % of peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
@@ -32,6 +34,31 @@ def raw(rep):
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}, vals[hdr.index("Kernel Name")]
+
+
+def fp64_flops(rep):
+    """FP64 flops of the captured launch from the SASS source page
+    (thread-level executed DFMA x2 + DMUL + DADD)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3 or "Source" not in rows[1]:
+        return None
+    hdr = rows[1]
+    i_src, i_thr = hdr.index("Source"), hdr.index("Thread Instructions Executed")
+    flops = 0
+    for r in rows[2:]:
+        if len(r) <= max(i_src, i_thr):
+            continue
+        toks = r[i_src].split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        op = op.split(".")[0]
+        w = {"DFMA": 2, "DMUL": 1, "DADD": 1}.get(op, 0)
+        if w:
+            flops += w * int(r[i_thr] or 0)
+    return float(flops)
 
 
 def stalls(d):
@@ -62,7 +89,14 @@ def main():
         try:
             tb = sum(float(d[k][0]) * UNIT[d[k][1]] for k in
                      ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            traffic[name.split("(")[0]] = tb
+            entry = {"dram_bytes": tb}
+            if "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active" in d:
+                entry["fp64_inst_pct_of_peak"] = float(
+                    d["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"][0])
+            fl = fp64_flops(rep)
+            if fl:
+                entry["fp64_flops"] = fl
+            traffic[name.split("(")[0]] = entry
         except (KeyError, ValueError):
             pass
         lines += [f"## `{name[:110]}`", "", f"report: `{rep}`", "",
