@@ -59,5 +59,15 @@ def main():
               f"loads {stats(release[:, k] - rel[:, k])}")
 
 
+    # which blocks publish last (sweep + intra-block skew), averaged over reductions
+    done = (pub[:, 2:min(ne, 12)] - release[:, 1:min(ne, 12) - 1]).mean(axis=1)
+    order = np.argsort(-done)
+    print("slowest blocks (mean release->publish us):",
+          ", ".join(f"{b}:{done[b] / 1e3:.2f}" for b in order[:12]))
+    print("fastest blocks:", ", ".join(f"{b}:{done[b] / 1e3:.2f}" for b in order[-6:]))
+    q = np.percentile(done, [10, 50, 90]) / 1e3
+    print(f"release->publish p10/p50/p90 {q[0]:.2f} {q[1]:.2f} {q[2]:.2f} us")
+
+
 if __name__ == "__main__":
     main()
