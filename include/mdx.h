@@ -190,6 +190,29 @@ int mdx_pcg_solve(const mdx_cg_args* args, int tissue, int blocks_hint, void* st
  * Rows [row_begin, row_end) of the local (owned + ghost) numbering. */
 int mdx_pcg_phase(const mdx_cg_args* args, int phase, int tissue, double alpha, double beta,
                   int first, int mbuf, double* sums_out, void* stream);
+
+/* Device-resident scalar state of the distributed pipelined PCG: the host
+ * enqueues phases without reading anything back; every rank's scalar
+ * kernel sees the same all-reduced sums and takes the same decisions
+ * (same formulas and order as the host driver, distributed.py). */
+typedef struct {
+  double b_norm, res, gamma, delta, gamma_prev, alpha_prev, alpha, beta, nonfinite;
+  int32_t it;     /* sweeps consumed */
+  int32_t state;  /* 0 iterating, 1 converged, 2 zero right-hand side, 3 max_iter reached */
+  int32_t first;  /* the next sweep is the first */
+  int32_t _pad;
+} mdx_pcg_scal;
+
+enum { MDX_SC_INIT = 0, MDX_SC_W0 = 1, MDX_SC_SWEEP = 2 };
+
+/* scal <- f(scal, sums) after phase MDX_SC_*: one thread, stream-ordered */
+int mdx_pcg_scalars(const double* sums, mdx_pcg_scal* scal, int phase, double tol,
+                    int max_iter, void* stream);
+/* mdx_pcg_phase with alpha/beta/first read from scal on the device; phases
+ * gate themselves on scal->state (w0/sweep only while iterating, x = 0 only
+ * for a zero right-hand side, activation only after a finite solve). */
+int mdx_pcg_phase_dev(const mdx_cg_args* args, int phase, int tissue, const mdx_pcg_scal* scal,
+                      int mbuf, double* sums_out, void* stream);
 /* y = A x with the same row arithmetic (csr_matvec, linalg.py:17-23) */
 int mdx_spmv(const mdx_cg_args* args, const double* x, double* y, void* stream);
 

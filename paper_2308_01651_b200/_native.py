@@ -73,6 +73,17 @@ class CgArgs(C.Structure):
     ]
 
 
+class PcgScal(C.Structure):
+    _fields_ = [
+        ("b_norm", _d), ("res", _d), ("gamma", _d), ("delta", _d), ("gamma_prev", _d),
+        ("alpha_prev", _d), ("alpha", _d), ("beta", _d), ("nonfinite", _d),
+        ("it", _i32), ("state", _i32), ("first", _i32), ("_pad", _i32),
+    ]
+
+
+SC_INIT, SC_W0, SC_SWEEP = 0, 1, 2
+
+
 class AssemblyArgs(C.Structure):
     _fields_ = [
         ("n_elem", _i64), ("nl", _i32), ("nq", _i32), ("nodes", _p),
@@ -110,6 +121,9 @@ _SIGNATURES = {
     "mdx_pcg_solve": ([C.POINTER(CgArgs), C.c_int, C.c_int, _p], C.c_int),
     "mdx_pcg_phase": ([C.POINTER(CgArgs), C.c_int, C.c_int, _d, _d, C.c_int, C.c_int, _p,
                        _p], C.c_int),
+    "mdx_pcg_phase_dev": ([C.POINTER(CgArgs), C.c_int, C.c_int, _p, C.c_int, _p, _p],
+                          C.c_int),
+    "mdx_pcg_scalars": ([_p, _p, C.c_int, _d, C.c_int, _p], C.c_int),
     "mdx_spmv": ([C.POINTER(CgArgs), _p, _p, _p], C.c_int),
     "mdx_assemble_local": ([C.POINTER(AssemblyArgs), _p], C.c_int),
     "mdx_scatter_csr": ([_i64, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],

@@ -22,6 +22,7 @@ logic over gloo with world size 2 and a CPU implementation of the hooks,
 against the single-domain oracle.
 """
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -113,20 +114,39 @@ class SlabComm:
         self.plan = slab.halo_plan()
 
     def halo(self, *vectors):
-        """Fill the ghost planes of each 1-D local vector from the neighbours."""
+        """Fill the ghost planes of each 1-D local vector from the neighbours.
+
+        NCCL moves device slices directly; gloo (CPU tests, or several ranks
+        sharing one GPU in the GPU tests) stages device slices through host
+        copies."""
         if not self.plan:
             return
         dist = self.dist
-        ops = []
+        staged = (dist.get_backend(self.group) == "gloo"
+                  and any(v.is_cuda for v in vectors))
+        ops, back = [], []
         for vec in vectors:
             for peer, (s0, s1), (r0, r1) in self.plan:
-                ops.append(dist.P2POp(dist.isend, vec[s0:s1], peer, group=self.group))
-                ops.append(dist.P2POp(dist.irecv, vec[r0:r1], peer, group=self.group))
+                snd, rcv = vec[s0:s1], vec[r0:r1]
+                if staged:
+                    snd = snd.cpu()
+                    host = rcv.cpu()
+                    back.append((rcv, host))
+                    rcv = host
+                ops.append(dist.P2POp(dist.isend, snd, peer, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, rcv, peer, group=self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        for dev, host in back:
+            dev.copy_(host)
 
     def allreduce(self, t):
         """Sum a small tensor over ranks in place; returns it."""
+        if t.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, group=self.group)
         return t
 
@@ -192,6 +212,66 @@ class PipelinedPcgDriver:
         return -self.max_iter, res / b_norm, nonfinite != 0.0
 
 
+class DevicePcgDriver:
+    """The same pipelined PCG with the scalar recurrences on the device.
+
+    Every phase, all-reduce, halo exchange and scalar update is enqueued on
+    the stream without reading anything back (NCCL collectives are
+    stream-ordered); the host reads the 88-byte scalar state only after a
+    chunk of iterations.  Phases enqueued after convergence are no-ops on the
+    device (they gate on the state), so the iterate is exactly the one the
+    host driver returns.  The first chunk is the previous solve's iteration
+    count, then chunks of two.
+
+    backend must provide phase_dev(kind, mbuf), scalars(phase) and
+    read_scalars(), plus the vectors PipelinedPcgDriver uses.
+    """
+
+    def __init__(self, comm, backend, tol, max_iter, predict=8):
+        self.comm = comm
+        self.be = backend
+        self.tol = float(tol)
+        self.max_iter = int(max_iter)
+        self.predict = max(1, int(predict))
+
+    def solve(self, tissue=True):
+        be, comm = self.be, self.comm
+        if tissue:
+            comm.halo(be.x, be.combo, *be.lift_currents())
+        else:
+            comm.halo(be.x)
+        be.phase_dev(PH_INIT)
+        comm.allreduce(be.sums)
+        be.scalars(N.SC_INIT)
+        be.phase_dev(PH_ZERO)
+        comm.halo(be.z)
+        be.phase_dev(PH_W0, mbuf=1)
+        comm.allreduce(be.sums)
+        be.scalars(N.SC_W0)
+        it, chunk = 0, self.predict
+        sc = None
+        while it < self.max_iter:
+            for _ in range(min(chunk, self.max_iter - it)):
+                it += 1
+                mbuf = (it - 1) & 1
+                comm.halo(be.m_buffer(mbuf))
+                be.phase_dev(PH_SWEEP, mbuf=mbuf)
+                comm.allreduce(be.sums)
+                be.scalars(N.SC_SWEEP)
+            sc = be.read_scalars()
+            if sc.state != 0:
+                break
+            chunk = 2
+        if sc is None:
+            sc = be.read_scalars()
+        if sc.state == 2:
+            return 0, 0.0, False
+        rel = sc.res / sc.b_norm
+        if sc.state == 1:
+            return sc.it, rel, sc.nonfinite != 0.0
+        return -self.max_iter, rel, sc.nonfinite != 0.0
+
+
 # ---------------------------------------------------------------------------
 # GPU backend + tissue solver
 # ---------------------------------------------------------------------------
@@ -205,7 +285,7 @@ class DistributedTissueSolver:
     each rank keeps only its slab of the vectors and ionic states.
     """
 
-    def __init__(self, config, group=None):
+    def __init__(self, config, group=None, device_scalars=True):
         import torch
         import torch.distributed as dist
 
@@ -214,6 +294,7 @@ class DistributedTissueSolver:
 
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
+        self.device_scalars = bool(device_scalars)
         lattice = detect_lattice(config.mesh)
         if lattice is None:
             raise ValueError("the distributed solver needs a structured hex slab")
@@ -263,6 +344,8 @@ class DistributedTissueSolver:
 
         self.ws = CgWorkspace(nl)
         self.sums = torch.zeros(4, **f64)
+        # device-resident PcgScal (88 bytes) for DevicePcgDriver
+        self.scal = torch.zeros(C.sizeof(N.PcgScal) // 8 + 1, **f64)
         self.tol = config.linear_solver.tolerance
         self.max_iter = config.linear_solver.max_iterations
         self.bdf_order = config.bdf_order
@@ -288,6 +371,19 @@ class DistributedTissueSolver:
                                       N.ptr(self.sums), N.stream_handle()), "mdx_pcg_phase")
         return self.sums.clone()
 
+    def phase_dev(self, kind, mbuf=0):
+        N.check(N.lib().mdx_pcg_phase_dev(N.C.byref(self._args), kind, 1, N.ptr(self.scal),
+                                          mbuf, N.ptr(self.sums), N.stream_handle()),
+                "mdx_pcg_phase_dev")
+
+    def scalars(self, phase):
+        N.check(N.lib().mdx_pcg_scalars(N.ptr(self.sums), N.ptr(self.scal), phase, self.tol,
+                                        self.max_iter, N.stream_handle()), "mdx_pcg_scalars")
+
+    def read_scalars(self):
+        raw = self.scal.cpu().numpy().tobytes()
+        return N.PcgScal.from_buffer_copy(raw[:C.sizeof(N.PcgScal)])
+
     # -- stepping (host logic shared with the CPU test backend) -----------------
     def step(self):
         from .simulation import RING_SLOTS
@@ -301,13 +397,21 @@ class DistributedTissueSolver:
         head, nslot = self.head, (self.head + 1) % RING_SLOTS
         self._ionic(order, t_next, head, nslot, mask)
         self._prepare_solve(order, t_next, head, nslot)
-        it, rel, nonfinite = PipelinedPcgDriver(self.comm, self, self.tol,
-                                                self.max_iter).solve(tissue=True)
+        if self.device_scalars:
+            it, rel, nonfinite = DevicePcgDriver(
+                self.comm, self, self.tol, self.max_iter,
+                predict=self.iters[-1] if self.iters else 8).solve(tissue=True)
+        else:
+            it, rel, nonfinite = PipelinedPcgDriver(self.comm, self, self.tol,
+                                                    self.max_iter).solve(tissue=True)
         if it < 0:
             raise SolverDivergence(-it, rel)
         if nonfinite:
             raise NonFiniteSolution("linear solve produced non-finite entries")
-        self.phase(PH_ACT)
+        if self.device_scalars:
+            self.phase_dev(PH_ACT)
+        else:
+            self.phase(PH_ACT)
         self.iters.append(it)
         self.head = nslot
         self.step_index += 1

@@ -29,10 +29,53 @@ def _wsum(vs, ws):
     return acc
 
 
+class _Scal:
+    """Fields of mdx_pcg_scal (include/mdx.h)."""
+
+    def __init__(self):
+        self.b_norm = self.res = self.gamma = self.delta = self.gamma_prev = 0.0
+        self.alpha_prev = self.alpha = self.beta = self.nonfinite = 0.0
+        self.it = self.state = self.first = 0
+
+
+def _scalars(s, c, phase, tol, max_iter):
+    """Restatement of pcg_scalars_kernel (csrc/solver.cu) for the CPU backend."""
+    if phase == 0:
+        c.b_norm, c.res, c.gamma, c.nonfinite = np.sqrt(s[0]), np.sqrt(s[1]), s[2], s[3]
+        c.it, c.first, c.gamma_prev, c.alpha_prev, c.alpha, c.beta = 0, 1, 0.0, 1.0, 0.0, 0.0
+        if c.b_norm == 0.0:
+            c.state, c.nonfinite, c.res = 2, 0.0, 0.0
+        elif c.res <= tol * c.b_norm:
+            c.state = 1
+        else:
+            c.state = 0
+    elif c.state == 0 and phase == 1:
+        c.delta, c.beta = s[0], 0.0
+        c.alpha = c.gamma / c.delta
+        c.first = 1
+        if max_iter < 1:
+            c.state = 3
+    elif c.state == 0 and phase == 2:
+        c.it += 1
+        c.nonfinite, c.res = s[3], np.sqrt(s[2])
+        if c.res <= tol * c.b_norm:
+            c.state = 1
+        elif c.it >= max_iter:
+            c.state = 3
+        else:
+            c.gamma_prev, c.alpha_prev, c.gamma, c.delta = c.gamma, c.alpha, s[0], s[1]
+            c.beta = c.gamma / c.gamma_prev
+            c.alpha = c.gamma / (c.delta - c.beta * c.gamma / c.alpha_prev)
+            c.first = 0
+
+
 class CpuSlabTissue(DistributedTissueSolver):
-    def __init__(self, config, group=None):
+    def __init__(self, config, group=None, device_scalars=False):
         import torch.distributed as dist
 
+        self.device_scalars = device_scalars
+        self.sums = torch.zeros(4, dtype=torch.float64)
+        self._scal = _Scal()
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
         self.slab = slab_partition(detect_lattice(config.mesh), self.nranks)[self.rank]
@@ -124,6 +167,26 @@ class CpuSlabTissue(DistributedTissueSolver):
 
     def _prepare_solve(self, order, t_next, head, nslot):
         self.x = self.u_ring[nslot]
+
+    # DevicePcgDriver protocol: the phases gate on the scalar state exactly as
+    # pcg_phase_kernel does with a non-null scal
+    def phase_dev(self, kind, mbuf=0):
+        c = self._scal
+        if kind in (PH_W0, PH_SWEEP) and c.state != 0:
+            return
+        if kind == PH_ZERO and c.state != 2:
+            return
+        if kind == PH_ACT and (c.state in (0, 3) or c.nonfinite != 0.0):
+            return
+        self.sums.copy_(self.phase(kind, c.alpha, c.beta, c.first, mbuf))
+
+    def scalars(self, phase):
+        _scalars(self.sums.numpy().copy(), self._scal, phase, self.tol, self.max_iter)
+
+    def read_scalars(self):
+        import copy
+
+        return copy.copy(self._scal)
 
     def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0):
         o0, o1 = self.o0, self.o1

@@ -75,6 +75,7 @@ STRUCTS = {
     "mdx_cg_args": "CgArgs",
     "mdx_assembly_args": "AssemblyArgs",
     "mdx_pace_args": "PaceArgs",
+    "mdx_pcg_scal": "PcgScal",
 }
 
 

@@ -44,7 +44,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, steps, out_dir):
+def _worker(rank, world, port, steps, out_dir, device_scalars=False):
     import sys
     from pathlib import Path
 
@@ -60,7 +60,7 @@ def _worker(rank, world, port, steps, out_dir):
         from paper_2308_01651_b200 import configs
 
         cfg = configs.config0(configs.this_package(), h=1e-3)
-        solver = CpuSlabTissue(cfg)
+        solver = CpuSlabTissue(cfg, device_scalars=device_scalars)
         for _ in range(steps):
             solver.step()
         u = solver.gather_potential()
@@ -75,14 +75,16 @@ def _worker(rank, world, port, steps, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_step_matches_single_domain_oracle(tmp_path, world):
+@pytest.mark.parametrize("world,device_scalars", [(2, False), (3, False), (2, True), (3, True)])
+def test_distributed_step_matches_single_domain_oracle(tmp_path, world, device_scalars):
+    """Host-driven (PipelinedPcgDriver) and device-scalar (DevicePcgDriver:
+    chunked enqueue, phases gated on the scalar state) distributed steps."""
     from oracle import monodomain_oracle as O
     from paper_2308_01651_b200 import configs
 
     steps = 60
-    mp.spawn(_worker, args=(world, _free_port(), steps, str(tmp_path)), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), steps, str(tmp_path), device_scalars),
+             nprocs=world, join=True)
     cfg = configs.config0(configs.this_package(), h=1e-3)
     orc = O.OracleTissue(cfg)
     for _ in range(steps):
