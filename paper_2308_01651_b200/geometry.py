@@ -11,7 +11,11 @@ against the reference vector for vector.
 
 Structured slabs additionally carry their lattice shape (`Mesh.lattice`), which
 is what lets the device use the class-table stencil operator instead of CSR.
-MSH/VTK file import/export is out of scope (host file I/O).
+`write_msh` / `import_msh` exchange meshes with the reference in its MSH 2.2
+ASCII dialect (`geometry.py:380-517`: 1-based ids, first physical tag =
+material id, lower-dimensional elements skipped) - SURVEY.md §8(f) item 3,
+so the reference can run the generated config-4 ventricle.  Other MSH
+versions and VTK import stay out of scope.
 """
 
 from dataclasses import dataclass, field
@@ -19,7 +23,7 @@ from enum import Enum
 
 import numpy as np
 
-from .errors import (DegenerateThickness, InvertedElement, NonDivisibleExtent,
+from .errors import (CorruptFile, DegenerateThickness, InvertedElement, NonDivisibleExtent,
                      ZeroSpacing)
 
 
@@ -236,3 +240,98 @@ def slab_fiber_field(mesh, transmural_axis, endo_angle, epi_angle):
     n0 = np.tile(e_n, (mesh.num_nodes, 1))
     s0 = np.cross(n0, f0)
     return FiberField(f0=f0, s0=s0, n0=n0).validate()
+
+
+# ---------------------------------------------------------------------------
+# MSH 2.2 ASCII exchange with the reference (geometry.py:380-517 there)
+# ---------------------------------------------------------------------------
+
+_MSH_TYPE = {ElementKind.TET4: 4, ElementKind.HEX8: 5}
+_MSH_KIND = {4: ElementKind.TET4, 5: ElementKind.HEX8}
+_MSH_LOWER_DIM = {1, 2, 3, 15}          # lines, triangles, quads, points: skipped
+
+
+def write_msh(mesh, path):
+    """MSH 2.2 ASCII: 1-based node/element ids, one physical tag (material id),
+    coordinates with 17 significant digits (round-trips fp64 exactly)."""
+    etype = _MSH_TYPE[mesh.element_kind]
+    n, e = mesh.num_nodes, mesh.num_elements
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n")
+        fh.write(f"$Nodes\n{n}\n")
+        ids = np.arange(1, n + 1)
+        np.savetxt(fh, np.column_stack([ids, mesh.nodes]), fmt=["%d", "%.17g", "%.17g", "%.17g"])
+        fh.write(f"$EndNodes\n$Elements\n{e}\n")
+        cols = np.column_stack([np.arange(1, e + 1), np.full(e, etype), np.ones(e, dtype=np.int64),
+                                mesh.material_ids.astype(np.int64),
+                                mesh.elements.astype(np.int64) + 1])
+        np.savetxt(fh, cols, fmt="%d")
+        fh.write("$EndElements\n")
+
+
+def import_msh(path, scaling_factor=1.0):
+    """Read an MSH 2.x ASCII volume mesh (tets or hexes, not mixed); the first
+    physical tag of each volume element becomes its material id.  Raises
+    CorruptFile on anything malformed."""
+    with open(path, encoding="ascii") as fh:
+        lines = fh.read().split("\n")
+
+    def section(name):
+        try:
+            a = lines.index(f"${name}")
+            b = lines.index(f"$End{name}", a)
+        except ValueError:
+            raise CorruptFile(f"MSH file lacks a ${name} section")
+        return lines[a + 1:b]
+
+    if "$MeshFormat" in lines and not section("MeshFormat")[0].split()[0].startswith("2."):
+        raise CorruptFile("only MSH format 2.x is supported")
+    body = section("Nodes")
+    try:
+        count = int(body[0])
+        tab = np.array([ln.split() for ln in body[1:count + 1]], dtype=np.float64)
+    except (ValueError, IndexError):
+        raise CorruptFile("malformed $Nodes section")
+    if tab.shape != (count, 4):
+        raise CorruptFile("node lines must be 'id x y z'")
+    node_ids = tab[:, 0].astype(np.int64)
+    order = np.argsort(node_ids)
+    if np.unique(node_ids).size != count:
+        raise CorruptFile("duplicate node ids")
+    body = section("Elements")
+    conn, tags, kind = [], [], None
+    try:
+        ecount = int(body[0])
+        rows = [ln.split() for ln in body[1:ecount + 1]]
+    except ValueError:
+        raise CorruptFile("malformed $Elements section")
+    for parts in rows:
+        etype, ntags = int(parts[1]), int(parts[2])
+        if etype in _MSH_LOWER_DIM:
+            continue
+        if etype not in _MSH_KIND:
+            raise CorruptFile(f"unsupported MSH element type {etype}")
+        k = _MSH_KIND[etype]
+        if kind is None:
+            kind = k
+        elif k is not kind:
+            raise CorruptFile("mesh mixes element types")
+        if ntags < 1:
+            raise CorruptFile("volume element without a physical tag")
+        tags.append(int(parts[3]))
+        conn.append([int(x) for x in parts[3 + ntags:]])
+    if kind is None:
+        raise CorruptFile("no volume elements")
+    conn = np.asarray(conn, dtype=np.int64)
+    if conn.shape[1] != NODES_PER_ELEMENT[kind]:
+        raise CorruptFile("wrong node count per element")
+    pos = np.searchsorted(node_ids[order], conn)
+    if (pos >= count).any() or (node_ids[order][np.minimum(pos, count - 1)] != conn).any():
+        raise CorruptFile("element references an unknown node id")
+    mesh = Mesh(tab[:, 1:] * float(scaling_factor), order[pos].astype(np.int32), kind,
+                np.asarray(tags, dtype=np.int32))
+    mesh.validate()
+    return mesh
+
+
+read_msh = import_msh

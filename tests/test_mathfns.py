@@ -18,7 +18,7 @@ SRC = (Path(__file__).resolve().parents[1] / "paper_2308_01651_b200" / "csrc"
 
 
 def _table(name):
-    m = re.search(r"__constant__ double " + name + r"\[64\] = \{(.*?)\};", SRC, re.S)
+    m = re.search(r"MDX_TABLE double " + name + r"\[64\] = \{(.*?)\};", SRC, re.S)
     return [float(x) for x in m.group(1).replace("\n", " ").split(",") if x.strip()]
 
 
