@@ -244,8 +244,8 @@ def run_ours(args):
     t0 = time.perf_counter()
     e2e_solver.restore(init_payload)
     for k in range(e2e_steps):
-        e2e_solver.enqueue_step()
-        e2e_solver.record_row(pidx, pinned[k])       # per-step D2H of the run() row
+        # the run() output row of every step, written by the solve into pinned host memory
+        e2e_solver.enqueue_step(record=(pidx, pinned[k]))
     e2e_solver.sync()
     barrier()
     assert np.isfinite(pinned.numpy()).all()

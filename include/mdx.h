@@ -179,6 +179,13 @@ typedef struct mdx_cg_args {
   /* distributed phases (mdx_pcg_phase): rows [row_begin, row_end) are the
      rank-owned local rows; 0/0 = all rows */
   int64_t row_begin, row_end;
+  /* optional run() output row of the solved potential, written by the solve
+     itself (mdx_pcg_solve, tissue=1): row_out = [min x, max x, x[row_probes]]
+     (device-accessible memory, e.g. mapped pinned host memory); NULL = none */
+  double* row_out;
+  const int64_t* row_probes;
+  int32_t row_nprobes;
+  int32_t _pad2;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */

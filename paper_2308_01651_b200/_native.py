@@ -70,6 +70,7 @@ class CgArgs(C.Structure):
         ("iters_out", _p), ("relres_out", _p), ("status", _p),
         ("fail_step", _p), ("variant", _i32), ("dom_class1", _i32),
         ("row_begin", _i64), ("row_end", _i64),
+        ("row_out", _p), ("row_probes", _p), ("row_nprobes", _i32), ("_pad2", _i32),
     ]
 
 

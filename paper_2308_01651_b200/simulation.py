@@ -517,11 +517,15 @@ class TissueSolver:
         self._slot_ptr = [N.ptr(self.u_ring[s]) for s in range(RING_SLOTS)]
         self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
 
-    def enqueue_step(self, events=None):
+    def enqueue_step(self, events=None, record=None):
         """Launch one step; no host synchronisation.
 
         `events`: optional (after_ionic, after_solve) CUDA events recorded on
         the launch stream (bench.py's per-kernel timing).
+        `record`: optional (probe_idx, dst): the solve itself writes the run()
+        output row [u_min, u_max, u[probes]] of the new potential into `dst`
+        (a pinned host float64 row, written through its device mapping, or a
+        CUDA tensor) - no extra kernel or copy.
         """
         import torch
 
@@ -564,7 +568,21 @@ class TissueSolver:
             self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
         a.iters_out = self._log_ptrs[0] + 4 * slot
         a.relres_out = self._log_ptrs[1] + 8 * slot
-        N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.blocks_hint, stream), "mdx_pcg_solve")
+        if record is not None:
+            probe_idx, dst = record
+            k = 2 + (0 if probe_idx is None else probe_idx.numel())
+            if not (dst.dtype == torch.float64 and dst.is_contiguous() and dst.numel() >= k
+                    and (dst.is_cuda or dst.is_pinned())):
+                raise ValueError("record row must be a contiguous float64 CUDA or pinned "
+                                 f"host tensor with >= {k} entries")
+            a.row_out = dst.data_ptr()
+            a.row_probes = N.ptr(probe_idx)
+            a.row_nprobes = 0 if probe_idx is None else probe_idx.numel()
+        try:
+            N.check(lib.mdx_pcg_solve(N.C.byref(a), 1, self.blocks_hint, stream),
+                    "mdx_pcg_solve")
+        finally:
+            a.row_out = None
         self.launches += 1
         if events is not None:
             events[1].record()
@@ -679,15 +697,24 @@ class TissueSolver:
         import torch
 
         k = 2 + (0 if probe_idx is None else probe_idx.numel())
-        if getattr(self, "_row_dev", None) is None or self._row_dev.numel() < k:
-            self._row_dev = torch.empty(k, dtype=torch.float64, device="cuda")
         if getattr(self, "_row_scratch", None) is None:
             self._row_scratch = torch.zeros(N.ROW_SCRATCH, dtype=torch.float64, device="cuda")
+        # pinned host memory is mapped into the device address space (UVA):
+        # the kernel writes the row straight into it, no copy is enqueued
+        direct = (not dst.is_cuda and dst.is_pinned() and dst.is_contiguous()
+                  and dst.dtype == torch.float64 and dst.numel() >= k)
+        if direct:
+            row = dst
+        else:
+            if getattr(self, "_row_dev", None) is None or self._row_dev.numel() < k:
+                self._row_dev = torch.empty(k, dtype=torch.float64, device="cuda")
+            row = self._row_dev
         N.check(N.lib().mdx_record_row(
             N.ptr(self.potential_device), self.n, N.ptr(probe_idx),
-            0 if probe_idx is None else probe_idx.numel(), N.ptr(self._row_dev),
+            0 if probe_idx is None else probe_idx.numel(), row.data_ptr(),
             N.ptr(self._row_scratch), N.stream_handle()), "mdx_record_row")
-        dst.copy_(self._row_dev[:k], non_blocking=True)
+        if not direct:
+            dst.copy_(self._row_dev[:k], non_blocking=True)
 
     def clamp_total(self):
         return int(self.clamps.item())
@@ -887,7 +914,15 @@ def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
 
     if solver.step_index == 0:
         record()
+    row_only = out.enable_csv or not out.enable_field_output
     while solver.step_index < n_steps:
+        k = solver.step_index + 1
+        if (k % out.stride == 0 or k == n_steps) and row_only and not out.enable_field_output:
+            # the row is written by the step's own solve kernel
+            with solver.timer.section("Other"):
+                solver.enqueue_step(record=(probe_idx, pinned[len(times)]))
+                times.append(solver.time)
+            continue
         solver.enqueue_step()
         k = solver.step_index
         if k % out.stride == 0 or k == n_steps:

@@ -488,6 +488,34 @@ def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path):
     assert _rel(res[0]["u"], g["snap_200"]) < 1e-9
 
 
+def test_fused_output_row(ns):
+    """enqueue_step(record=...): the solve kernel writes [min, max, probes] of
+    the new potential into pinned host memory (resident stencil kernel on a
+    slab, grid-stride SELL kernel on tets) - same values as the standalone
+    record_row kernel and as the potential itself."""
+    import torch
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    for cfg in (configs.config0(ns), configs.config0(ns, kind="Tet4")):
+        s = TissueSolver(cfg)
+        probes = torch.tensor([0, 7, s.n // 2, s.n - 1], device="cuda")
+        fused = torch.zeros((40, 6), dtype=torch.float64, pin_memory=True)
+        alone = torch.zeros((40, 6), dtype=torch.float64, pin_memory=True)
+        pots = []
+        for k in range(40):
+            s.enqueue_step(record=(probes, fused[k]))
+            s.record_row(probes, alone[k])
+            pots.append(s.potential_device.clone())
+        s.sync()
+        for k in range(40):
+            u = pots[k].cpu().numpy()
+            want = [u.min(), u.max(), *u[probes.cpu().numpy()]]
+            np.testing.assert_array_equal(fused[k].numpy(), want)
+            np.testing.assert_array_equal(alone[k].numpy(), want)
+
+
 def test_cfg4_ventricle_small(golden, ns):
     """Config-4 geometry (prolate-spheroid P1 tets, helix fibers, endo/mid/epi
     volumes with duplicated interface states) on a reduced grid, CSR path."""
