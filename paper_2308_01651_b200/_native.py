@@ -27,6 +27,7 @@ OP_CSR = 2
 OP_SELL = 3
 ROW_SCRATCH = 1024        # MDX_ROW_SCRATCH
 MAX_LIFT = 8
+ABI_VERSION = 2   # include/mdx.h MDX_ABI_VERSION
 
 STATUS_DIVERGED = 1
 STATUS_NONFINITE = 2
@@ -71,6 +72,7 @@ class CgArgs(C.Structure):
         ("fail_step", _p), ("variant", _i32), ("dom_class1", _i32),
         ("row_begin", _i64), ("row_end", _i64),
         ("row_out", _p), ("row_probes", _p), ("row_nprobes", _i32), ("_pad2", _i32),
+        ("dom_row_host", _p), ("ll_halo", _p),
     ]
 
 
@@ -166,7 +168,7 @@ def lib():
                 "no CUDA device: the monodomain kernels run only on sm_100a "
                 "(there is no CPU fallback)")
         _lib = load_library()
-        if _lib.mdx_abi_version() != 1:
+        if _lib.mdx_abi_version() != ABI_VERSION:
             raise NativeUnavailable("libmdx.so ABI version mismatch")
     return _lib
 

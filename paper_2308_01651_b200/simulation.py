@@ -513,6 +513,12 @@ class TissueSolver:
             a.dom_class1 = 0
         self._cg_args = a
         self._a_ptr = {k: N.ptr(v) for k, v in op.a_tables.items()}
+        # host copy of the dominant class row per BDF order (brick solver)
+        self._dom_host = {}
+        if a.dom_class1 > 0 and hasattr(op, "host_a"):
+            for k, tab in op.host_a.items():
+                self._dom_host[k] = np.ascontiguousarray(tab[a.dom_class1 - 1], np.float64)
+        self._dom_ptr = {k: v.ctypes.data for k, v in self._dom_host.items()}
         self._dinv_ptr = {k: N.ptr(v) for k, v in op.dinv.items()}
         self._slot_ptr = [N.ptr(self.u_ring[s]) for s in range(RING_SLOTS)]
         self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
@@ -558,6 +564,7 @@ class TissueSolver:
         a = self._cg_args
         a.a_val = self._a_ptr[order]
         a.dinv = self._dinv_ptr[order]
+        a.dom_row_host = self._dom_ptr.get(order)
         a.step = self.step_index
         a.x = self._slot_ptr[nslot]
         a.u_prev = self._slot_ptr[head]
