@@ -187,12 +187,9 @@ typedef struct mdx_cg_args {
   int32_t row_nprobes;
   int32_t _pad2;
   /* optional HOST copy of the 27 coefficients of class dom_class1 - 1 of
-     a_val (the structured brick solver passes them as kernel parameters);
+     a_val (the brick-streaming solver passes them as kernel parameters);
      read at launch time only; NULL = use the device table */
   const double* dom_row_host;
-  /* LL exchange words of the structured column solver: 4 n zero-initialised
-     uint64 (two buffers of [n][2]); NULL = that solver is not used */
-  unsigned long long* ll_halo;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */

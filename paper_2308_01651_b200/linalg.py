@@ -39,8 +39,6 @@ class CgWorkspace:
         self.w = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.s = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         self.m = torch.zeros(2 * max(n, 1), dtype=torch.float64, device="cuda")
-        # LL exchange words of the structured column solver (two [n][2] buffers)
-        self.ll_halo = torch.zeros(4 * max(n, 1), dtype=torch.int64, device="cuda")
         self.iters = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.relres = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -57,7 +55,6 @@ class CgWorkspace:
         a.w = N.ptr(self.w)
         a.s = N.ptr(self.s)
         a.m = N.ptr(self.m)
-        a.ll_halo = N.ptr(self.ll_halo)
         a.iters_out = N.ptr(self.iters)
         a.relres_out = N.ptr(self.relres)
         a.status = N.ptr(self.status)

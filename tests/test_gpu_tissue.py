@@ -554,3 +554,25 @@ def test_run_loop_rows_csv_and_vtk(golden, ns, tmp_path):
     assert (tmp_path / "act.vtk").read_text().startswith("# vtk DataFile Version 3.0")
     assert rep.max_cg_iterations == int(g["iters"][:100].max()) or \
         abs(rep.max_cg_iterations - int(g["iters"][:100].max())) <= 1
+
+
+def test_stream_kernel_parity(tmp_path):
+    """The brick-streaming solver (MDX_PCG_KERNEL=stream, chosen once per
+    process) against the reference goldens: config 0 (BO, full 800 steps),
+    the TTP06 slab and config 2 at full size, in a child pytest."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MDX_PCG_KERNEL="stream", MDX_DEBUG_PLAN="1")
+    sel = "cfg0_bo_full_run or test_ttp06_slab or cfg2_full_size_head"
+    res = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-s", "-m", "gpu",
+                          "-k", sel, "-p", "no:cacheprovider", __file__],
+                         env=env, capture_output=True, text=True, timeout=900)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert "[mdx] stream plan" in out, out[-2000:]
+    import re
+
+    m = re.search(r"(\d+) passed", out)
+    assert m and int(m.group(1)) >= 3 and " failed" not in out, out[-2000:]
