@@ -157,41 +157,56 @@ tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
   if (a.status && *(volatile const int32_t*)a.status) return;
   const Bdf b = bdf_of(ORDER);
   const int S = a.ring_slots;
+  const int nslot = (a.head + 1) % S;
+  // ring slots of this step, resolved once: u and W history bases (newest
+  // first) and the slot W_{n+1} goes to; a node then walks its variables with
+  // one pointer increment per access
+  const double* ub[ORDER];
+  const double* wbase[ORDER];
+#pragma unroll
+  for (int k = 0; k < ORDER; ++k) {
+    const int slot = (a.head - k + 3 * S) % S;
+    ub[k] = a.u_ring + (int64_t)slot * a.ldu;
+    wbase[k] = a.w_ring + (int64_t)slot * M::NV * a.ldw;
+  }
+  double* const wout = a.w_ring + (int64_t)nslot * M::NV * a.ldw;
+  const int64_t ldw = a.ldw;
   int local_clamp = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t node = a.dofs ? (int64_t)a.dofs[i] : i;
     double uh[ORDER];
 #pragma unroll
-    for (int k = 0; k < ORDER; ++k) {
-      const int slot = (a.head - k + 3 * S) % S;
-      uh[k] = a.u_ring[slot * a.ldu + node];
-    }
+    for (int k = 0; k < ORDER; ++k) uh[k] = ub[k][node];
     const double u_ext = combine<ORDER>(uh, b.e);
 
-    const int nslot = (a.head + 1) % S;
-    auto hist = [&](int v, const double* wts) {
-      double wh[ORDER];
-#pragma unroll
-      for (int k = 0; k < ORDER; ++k) {
-        const int slot = (a.head - k + 3 * S) % S;
-        wh[k] = a.w_ring[((int64_t)slot * M::NV + v) * a.ldw + i];
-      }
-      return combine<ORDER>(wh, wts);
-    };
-    auto store = [&](int v, double x) {
-      a.w_ring[((int64_t)nslot * M::NV + v) * a.ldw + i] = x;
-    };
     double I;
     double we[M::NV], wb[M::NV], wo[M::NV];
+    {
+      const double* p[ORDER];
 #pragma unroll
-    for (int v = 0; v < M::NV; ++v) {
-      wb[v] = hist(v, b.h);
-      we[v] = M::NEEDS_WEXT ? hist(v, b.e) : 0.0;
+      for (int k = 0; k < ORDER; ++k) p[k] = wbase[k] + i;
+#pragma unroll
+      for (int v = 0; v < M::NV; ++v) {
+        double wh[ORDER];
+#pragma unroll
+        for (int k = 0; k < ORDER; ++k) {
+          wh[k] = *p[k];
+          p[k] += ldw;
+        }
+        wb[v] = combine<ORDER>(wh, b.h);
+        we[v] = M::NEEDS_WEXT ? combine<ORDER>(wh, b.e) : 0.0;
+      }
     }
     M::advance(u_ext, we, wb, b.alpha, a.dt, P, wo, I, local_clamp);
+    {
+      double* po = wout + i;
 #pragma unroll
-    for (int v = 0; v < M::NV; ++v) store(v, wo[v]);
+      for (int v = 0; v < M::NV; ++v) {
+        *po = wo[v];
+        po += ldw;
+      }
+    }
     a.i_out[node] = I;
 
     if (a.prep) {
