@@ -338,6 +338,7 @@ def run_distributed(args, cfg, n, rank, world, local, dist):
         solver.step()
     dist.barrier()
     torch.cuda.synchronize()
+    launches0 = solver.launches
     with ClockSampler(local) as clocks:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -363,7 +364,7 @@ def run_distributed(args, cfg, n, rank, world, local, dist):
                        "cg_iters_per_step": [int(its.min()), float(its.mean()),
                                              int(its.max())]},
             "clocks": clocks.summary(),
-            "gpu_launches": None,
+            "gpu_launches": solver.launches - launches0,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

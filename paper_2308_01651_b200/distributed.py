@@ -295,6 +295,7 @@ class DistributedTissueSolver:
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
         self.device_scalars = bool(device_scalars)
+        self.launches = 0          # libmdx kernels enqueued (bench.py's gpu_launches)
         lattice = detect_lattice(config.mesh)
         if lattice is None:
             raise ValueError("the distributed solver needs a structured hex slab")
@@ -369,16 +370,19 @@ class DistributedTissueSolver:
         a = self._args
         N.check(N.lib().mdx_pcg_phase(N.C.byref(a), kind, 1, alpha, beta, first, mbuf,
                                       N.ptr(self.sums), N.stream_handle()), "mdx_pcg_phase")
+        self.launches += 2          # phase kernel + partial reduction
         return self.sums.clone()
 
     def phase_dev(self, kind, mbuf=0):
         N.check(N.lib().mdx_pcg_phase_dev(N.C.byref(self._args), kind, 1, N.ptr(self.scal),
                                           mbuf, N.ptr(self.sums), N.stream_handle()),
                 "mdx_pcg_phase_dev")
+        self.launches += 2
 
     def scalars(self, phase):
         N.check(N.lib().mdx_pcg_scalars(N.ptr(self.sums), N.ptr(self.scal), phase, self.tol,
                                         self.max_iter, N.stream_handle()), "mdx_pcg_scalars")
+        self.launches += 1
 
     def read_scalars(self):
         raw = self.scal.cpu().numpy().tobytes()
@@ -436,6 +440,7 @@ class DistributedTissueSolver:
         Ph, Pp = N.host_doubles(self.packed)
         N.check(N.lib().mdx_tissue_ionic(self.model_id, N.C.byref(ia), Pp, int(Ph.size),
                                          N.stream_handle()), "mdx_tissue_ionic")
+        self.launches += 1
 
     def _prepare_solve(self, order, t_next, head, nslot):
         sl = self.slab
