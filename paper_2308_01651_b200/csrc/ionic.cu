@@ -14,10 +14,12 @@
 #include "common.cuh"
 #include "ionic_models.cuh"
 
-// 4 x 128 threads per SM caps registers at 128 (a few spills): 4 warps per
-// SM sub-partition beat 3 warps at 168 spill-free registers by ~3%
+// 3 x 128 threads per SM: 168 registers, no spills.  Since the kernel lost
+// its inlined library log and per-variable index math, 3 spill-free warps per
+// SM sub-partition beat 4 at 128 registers (76.8 vs 78.1 us on config 2) and
+// 5 at 96 (83.1 us)
 #ifndef MDX_IONIC_MINB
-#define MDX_IONIC_MINB 4
+#define MDX_IONIC_MINB 3
 #endif
 #ifndef MDX_IONIC_BLOCK
 #define MDX_IONIC_BLOCK 128
