@@ -137,8 +137,18 @@ __device__ __forceinline__ Bdf bdf_of(int order) {
   return b;
 }
 
+// BDF1/BDF2 weights are 1, 2, -1/2, -1: every product is exact, so the FMA
+// form rounds once exactly where the reference's separately rounded
+// multiply-then-add does (bitwise equal), costs half the FP64 work, and lets
+// the compiler share 2*w_n between the BDF and the extrapolation sums.
 template <int ORDER>
 __device__ __forceinline__ double combine(const double (&x)[ORDER], const double* wts) {
+  if (ORDER <= 2) {
+    double acc = wts[0] * x[0];
+#pragma unroll
+    for (int k = 1; k < ORDER; ++k) acc = fma(wts[k], x[k], acc);
+    return acc;
+  }
   double acc = mul_rn(wts[0], x[0]);
 #pragma unroll
   for (int k = 1; k < ORDER; ++k) acc = madd_rn(acc, wts[k], x[k]);
