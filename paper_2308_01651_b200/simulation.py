@@ -761,10 +761,19 @@ class TissueSolver:
         return b"".join(parts)
 
     def restore(self, payload):
+        """Load a checkpoint payload (the reference's MHEP body).  `payload` is
+        bytes-like, or a uint8 CPU tensor - in pinned memory the upload is one
+        asynchronous DMA instead of a staged pageable copy."""
         import torch
 
         if self._pending:
             self.sync()
+        src = None
+        if isinstance(payload, torch.Tensor):
+            if payload.dtype != torch.uint8 or payload.dim() != 1 or payload.is_cuda:
+                raise ValueError("a tensor payload must be a 1-D uint8 CPU tensor")
+            src = payload
+            payload = payload.numpy()
         version, n = struct.unpack_from("<IQ", payload, 0)
         if version != CHECKPOINT_VERSION:
             raise VersionMismatch(f"checkpoint version {version}, expected "
@@ -814,10 +823,13 @@ class TissueSolver:
             raise CorruptFile("checkpoint payload truncated")
         import warnings
 
-        with warnings.catch_warnings():          # read-only bytes: never written
-            warnings.simplefilter("ignore", UserWarning)
-            raw = torch.frombuffer(payload, dtype=torch.uint8, count=off)
-        dev = raw.to("cuda")
+        if src is not None:
+            dev = src[:off].to("cuda", non_blocking=src.is_pinned())
+        else:
+            with warnings.catch_warnings():      # read-only bytes: never written
+                warnings.simplefilter("ignore", UserWarning)
+                raw = torch.frombuffer(payload, dtype=torch.uint8, count=off)
+            dev = raw.to("cuda")
         tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8}
 
         def seg(k):

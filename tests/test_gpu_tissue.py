@@ -576,3 +576,29 @@ def test_stream_kernel_parity(tmp_path):
 
     m = re.search(r"(\d+) passed", out)
     assert m and int(m.group(1)) >= 3 and " failed" not in out, out[-2000:]
+
+
+def test_restore_from_pinned_tensor(ns):
+    """restore() from a pinned uint8 tensor (one async DMA) = restore from bytes."""
+    import torch
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = configs.config0(ns, h=1e-3)
+    s = TissueSolver(cfg)
+    for _ in range(7):
+        s.step(return_potential=False)
+    s.sync()
+    payload = s.checkpoint_payload()
+    a, b = TissueSolver(cfg), TissueSolver(cfg)
+    a.restore(payload)
+    b.restore(torch.frombuffer(bytearray(payload), dtype=torch.uint8).pin_memory())
+    for _ in range(5):
+        a.step(return_potential=False)
+        b.step(return_potential=False)
+    a.sync()
+    b.sync()
+    assert np.array_equal(a.potential, b.potential)
+    assert np.array_equal(a.activation_map, b.activation_map)
+    assert a.step_index == b.step_index == 12
