@@ -287,7 +287,7 @@ def run_ours(args):
                               "frac": flops / ionic_avg / 1e12 / fp64_peak,
                               "flops_per_launch": flops}
     t_pcg = traffic_of("pcg_resident_kernel") or traffic_of("pcg_kernel")
-    roof_pcg = {"bound": "hbm", "kernel": "pcg_resident_kernel<tissue,3> (vectors in SMEM: "
+    roof_pcg = {"bound": "hbm", "kernel": "pcg_resident_kernel<tissue,4> (vectors in SMEM: "
                 "HBM roofline of the unfused algorithm's bytes)",
                 "achieved": pcg_achieved, "peak": hbm, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": pcg_achieved / hbm,
