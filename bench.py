@@ -132,6 +132,9 @@ def dist_env():
     return rank, world, local
 
 
+PLATEAU_STEP = 2500          # t = 50 ms at dt = 2e-5 s: every node depolarised
+
+
 def cpu_sample(steps, threads=None, warmup=2):
     """Oracle port of the reference step on cfg 2: `warmup` (>= 2, the BDF
     start-up) untimed steps from rest, then `steps` timed steps."""
@@ -234,6 +237,33 @@ def run_ours(args):
     its = solver.iterations_log()[-args.steps:]
     solver.sync()
 
+    # ---- plateau phase (reported beside the headline) ------------------------
+    # the propagation phase is CG-bound, the plateau (every node
+    # depolarised, CG 1-2 iterations) ionic/FP64-bound.  The same solver is
+    # advanced untimed to t = 50 ms, then K steps are device-timed again.
+    plateau = None
+    if world == 1 and not args.no_plateau:
+        while solver.step_index < PLATEAU_STEP:
+            solver.enqueue_step()
+        solver.sync()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        p0.record()
+        for _ in range(args.steps):
+            solver.enqueue_step()
+        p1.record()
+        barrier()
+        pms = p0.elapsed_time(p1)
+        pits = solver.iterations_log()[-args.steps:]
+        solver.sync()
+        plateau = {"value": n * args.steps / (pms * 1e-3), "unit": UNIT,
+                   "ms_per_step": pms / args.steps, "from_step": PLATEAU_STEP,
+                   "cg_iters_per_step": [int(pits.min()), float(pits.mean()), int(pits.max())],
+                   "bytes_per_step_frac_hbm": float(
+                       n * (562 + 104 * pits.astype(np.float64)).sum()
+                       / (pms * 1e-3) / 1e9 / peaks()[0])}
+
     # ---- end-to-end through the public API ----------------------------------
     e2e_solver = TissueSolver(cfg)
     probes = [ns.nearest_node(cfg.mesh, p) for p in configs.corner_probes()]
@@ -314,6 +344,9 @@ def run_ours(args):
         "roofline": roof_pcg if dominant_pcg else roof_ionic,
         "roofline_other": roof_ionic if dominant_pcg else roof_pcg,
         "roofline_step": roof_step,
+        "phases": {"propagation": {"value": n * args.steps * world / (ms * 1e-3),
+                                   "from_step": args.warmup},
+                   "plateau": plateau},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": len(init_payload) / e2e_steps,
                 "d2h_bytes_per_step": 8 * (2 + len(probes))},
@@ -378,6 +411,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--no-plateau", action="store_true",
+                    help="skip the plateau-phase sample (t = 50 ms) of the same run")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
