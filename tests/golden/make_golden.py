@@ -210,7 +210,7 @@ def _drive(solver, steps, probes, snap_every=None, payload_at=()):
     return its, pr, umin, umax, snaps, payloads, wall
 
 
-def tissue(name, build, steps, snap_every=None, payload_at=(), subsample=None):
+def tissue(name, build, steps, snap_every=None, payload_at=(), subsample=None, lean=False):
     configs, ns = _ref()
     from monodomain.simulation import TissueSolver
 
@@ -228,8 +228,10 @@ def tissue(name, build, steps, snap_every=None, payload_at=(), subsample=None):
                                                         snap_every, payload_at)
     out = dict(iters=its, probes=np.asarray(probes), probe_u=pr, umin=umin, umax=umax,
                steps=np.array(steps), wall=np.array(wall),
-               activation=solver.activation_map, best_slope=solver.best_slope,
-               frozen=solver.frozen.astype(np.uint8))
+               activation=solver.activation_map)
+    out["frozen"] = solver.frozen.astype(np.uint8)
+    if not lean:               # lean: full-size fixtures drop the best-slope field
+        out["best_slope"] = solver.best_slope
     u = solver.potential
     out["final_u_sha"] = np.array(sha(u))
     if subsample:
@@ -319,6 +321,10 @@ JOBS = {
         snap_every=500),
     "tissue_cfg2_head": lambda: tissue("tissue_cfg2_head", lambda c, ns: c.config2(ns),
                                        40, snap_every=20, subsample=97),
+    # config 2 at full size through the first 10 ms of propagation: iteration
+    # counts, probe traces and the full activation map of ~1/4 of the slab
+    "tissue_cfg2_500": lambda: tissue("tissue_cfg2_500", lambda c, ns: c.config2(ns),
+                                      500, subsample=97, lean=True),
 }
 
 if __name__ == "__main__":

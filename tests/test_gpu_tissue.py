@@ -305,6 +305,31 @@ def test_cfg2_full_size_head(golden, ns):
     assert s.op.ncls == 27          # uniform slab: interior + 26 boundary classes
 
 
+def test_cfg2_full_size_500_steps(golden, ns):
+    """Config 2 at full size (442,401 nodes) through 10 ms of propagation (500
+    steps) against the reference: CG iterations within +-1, probe traces, the
+    set of activated (threshold-crossed) nodes and their activation times
+    within one time step."""
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg2_500")
+    dt = 2e-5
+    s, pu = _run_against(g, configs.config2(ns), 500)
+    its = s.iterations_log()
+    assert np.abs(its - g["iters"]).max() <= 1
+    assert (its == g["iters"]).mean() > 0.95
+    assert _rel(pu, g["probe_u"]) < 1e-6          # BASELINE bar (measured ~1e-9)
+    sub = int(g["subsample"])
+    assert _rel(s.potential[::sub], g["final_u_sub"]) < 1e-6
+    fz, rfz = s.frozen.cpu().numpy().astype(bool), g["frozen"].astype(bool)
+    assert rfz.sum() > 10000                       # the front has swept a good part
+    # nodes crossing the threshold at the very last steps may differ by one step
+    assert (fz != rfz).sum() <= 1e-3 * rfz.sum()
+    both = fz & rfz
+    act, ref = s.activation_map, g["activation"]
+    assert np.abs(act[both] - ref[both]).max() <= dt * (1 + 1e-9)
+
+
 def test_checkpoint_format_and_cross_restore(golden, ns):
     """Restore the REFERENCE's checkpoint (step 400) and continue to 800."""
     from paper_2308_01651_b200 import configs
