@@ -24,6 +24,7 @@ against the single-domain oracle.
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -82,6 +83,29 @@ class LocalSlab:
         return plan
 
 
+    def sweep_split(self):
+        """((i0, i1), [boundary ranges]) of the owned local rows, or None.
+
+        Interior rows have no ghost-plane neighbour (the 27-point row of a
+        node in plane k reads planes k-1..k+1), so their CG sweep can run
+        while the halo exchange of m is in flight; the boundary planes next to
+        a ghost plane run after it lands.  None: no halo, or no interior."""
+        P = self.plane
+        lo = P if self.k0 > 0 else 0
+        hi = P if self.k1 < self.nz1 else 0
+        if not (lo or hi):
+            return None
+        i0, i1 = self.own_begin + lo, self.own_end - hi
+        if i1 <= i0:
+            return None
+        bnd = []
+        if lo:
+            bnd.append((self.own_begin, i0))
+        if hi:
+            bnd.append((i1, self.own_end))
+        return (i0, i1), bnd
+
+
 def slab_partition(lattice, nranks):
     """Split the node planes of an (nx, ny, nz)-cell lattice into nranks slabs
     of near-equal plane counts (z-planes, contiguous in node numbering)."""
@@ -114,13 +138,19 @@ class SlabComm:
         self.plan = slab.halo_plan()
 
     def halo(self, *vectors):
-        """Fill the ghost planes of each 1-D local vector from the neighbours.
+        """Fill the ghost planes of each 1-D local vector from the neighbours."""
+        self.halo_finish(self.halo_start(*vectors))
 
-        NCCL moves device slices directly; gloo (CPU tests, or several ranks
-        sharing one GPU in the GPU tests) stages device slices through host
-        copies."""
+    def halo_start(self, *vectors):
+        """Post the halo sends/receives; returns the pending exchange.
+
+        NCCL moves device slices directly and its work runs on NCCL's stream
+        (ordered after the work already enqueued on the current stream), so
+        kernels enqueued before halo_finish overlap the transfer.  gloo (CPU
+        tests, or several ranks sharing one GPU in the GPU tests) stages device
+        slices through host copies."""
         if not self.plan:
-            return
+            return None
         dist = self.dist
         staged = (dist.get_backend(self.group) == "gloo"
                   and any(v.is_cuda for v in vectors))
@@ -135,7 +165,16 @@ class SlabComm:
                     rcv = host
                 ops.append(dist.P2POp(dist.isend, snd, peer, group=self.group))
                 ops.append(dist.P2POp(dist.irecv, rcv, peer, group=self.group))
-        for req in dist.batch_isend_irecv(ops):
+        return dist.batch_isend_irecv(ops), back
+
+    def halo_finish(self, pending):
+        """Complete a halo_start: NCCL makes the current stream wait for the
+        transfer (no host block); gloo waits on the host and copies staged
+        receives back to the device."""
+        if pending is None:
+            return
+        reqs, back = pending
+        for req in reqs:
             req.wait()
         for dev, host in back:
             dev.copy_(host)
@@ -154,6 +193,14 @@ class SlabComm:
 # ---------------------------------------------------------------------------
 # Backend-agnostic pipelined PCG driver
 # ---------------------------------------------------------------------------
+
+
+def _sweep_split(be):
+    """The backend's interior/boundary row split for halo overlap, or None
+    (no neighbours, no interior, or MDX_DIST_OVERLAP=0)."""
+    if os.environ.get("MDX_DIST_OVERLAP", "1") == "0":
+        return None
+    return be.slab.sweep_split()
 
 
 class PipelinedPcgDriver:
@@ -202,8 +249,20 @@ class PipelinedPcgDriver:
                 beta = gamma / gamma_prev
                 alpha = gamma / (delta - beta * gamma / alpha_prev)
             mbuf = (it - 1) & 1
-            comm.halo(be.m_buffer(mbuf))
-            s = self._sums(be.phase(PH_SWEEP, alpha, beta, int(first), mbuf))
+            split = _sweep_split(be)
+            if split is None:
+                comm.halo(be.m_buffer(mbuf))
+                local = be.phase(PH_SWEEP, alpha, beta, int(first), mbuf)
+            else:
+                # interior rows while the halo of m is in flight, then the
+                # planes next to the ghosts; local sums in a fixed order
+                pend = comm.halo_start(be.m_buffer(mbuf))
+                local = be.phase(PH_SWEEP, alpha, beta, int(first), mbuf, rows=split[0])
+                comm.halo_finish(pend)
+                for rows in split[1]:
+                    local = local + be.phase(PH_SWEEP, alpha, beta, int(first), mbuf,
+                                             rows=rows)
+            s = self._sums(local)
             nonfinite = s[3]
             res = math.sqrt(s[2])
             if res <= self.tol * b_norm:
@@ -250,12 +309,22 @@ class DevicePcgDriver:
         be.scalars(N.SC_W0)
         it, chunk = 0, self.predict
         sc = None
+        split = _sweep_split(be)
         while it < self.max_iter:
             for _ in range(min(chunk, self.max_iter - it)):
                 it += 1
                 mbuf = (it - 1) & 1
-                comm.halo(be.m_buffer(mbuf))
-                be.phase_dev(PH_SWEEP, mbuf=mbuf)
+                if split is None:
+                    comm.halo(be.m_buffer(mbuf))
+                    be.phase_dev(PH_SWEEP, mbuf=mbuf)
+                else:
+                    # interior rows overlap the halo exchange of m
+                    pend = comm.halo_start(be.m_buffer(mbuf))
+                    be.phase_dev(PH_SWEEP, mbuf=mbuf, rows=split[0], part=0)
+                    comm.halo_finish(pend)
+                    for j, rows in enumerate(split[1]):
+                        be.phase_dev(PH_SWEEP, mbuf=mbuf, rows=rows, part=j + 1)
+                    be.combine_parts(1 + len(split[1]))
                 comm.allreduce(be.sums)
                 be.scalars(N.SC_SWEEP)
             sc = be.read_scalars()
@@ -345,6 +414,7 @@ class DistributedTissueSolver:
 
         self.ws = CgWorkspace(nl)
         self.sums = torch.zeros(4, **f64)
+        self.sum_parts = torch.zeros((3, 4), **f64)   # interior + two boundary planes
         # device-resident PcgScal (88 bytes) for DevicePcgDriver
         self.scal = torch.zeros(C.sizeof(N.PcgScal) // 8 + 1, **f64)
         self.tol = config.linear_solver.tolerance
@@ -366,18 +436,35 @@ class DistributedTissueSolver:
     def z(self):
         return self.ws.z
 
-    def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0):
+    def _rows_args(self, rows):
+        """The solve's kernel arguments, restricted to local rows [r0, r1)."""
         a = self._args
+        if rows is None:
+            return a
+        b = N.CgArgs.from_buffer_copy(a)
+        b.row_begin, b.row_end = rows
+        return b
+
+    def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0, rows=None):
+        a = self._rows_args(rows)
         N.check(N.lib().mdx_pcg_phase(N.C.byref(a), kind, 1, alpha, beta, first, mbuf,
                                       N.ptr(self.sums), N.stream_handle()), "mdx_pcg_phase")
         self.launches += 2          # phase kernel + partial reduction
         return self.sums.clone()
 
-    def phase_dev(self, kind, mbuf=0):
-        N.check(N.lib().mdx_pcg_phase_dev(N.C.byref(self._args), kind, 1, N.ptr(self.scal),
-                                          mbuf, N.ptr(self.sums), N.stream_handle()),
-                "mdx_pcg_phase_dev")
+    def phase_dev(self, kind, mbuf=0, rows=None, part=None):
+        """part j: the local sums go to sum_parts[j] (combine_parts adds them)."""
+        out = self.sums if part is None else self.sum_parts[part]
+        N.check(N.lib().mdx_pcg_phase_dev(N.C.byref(self._rows_args(rows)), kind, 1,
+                                          N.ptr(self.scal), mbuf, N.ptr(out),
+                                          N.stream_handle()), "mdx_pcg_phase_dev")
         self.launches += 2
+
+    def combine_parts(self, k):
+        """sums = sum_parts[0] + ... + sum_parts[k-1] (fixed order)."""
+        import torch
+
+        torch.sum(self.sum_parts[:k], 0, out=self.sums)
 
     def scalars(self, phase):
         N.check(N.lib().mdx_pcg_scalars(N.ptr(self.sums), N.ptr(self.scal), phase, self.tol,

@@ -75,6 +75,8 @@ class CpuSlabTissue(DistributedTissueSolver):
 
         self.device_scalars = device_scalars
         self.sums = torch.zeros(4, dtype=torch.float64)
+        self.sum_parts = torch.zeros((3, 4), dtype=torch.float64)
+        self.sweep_rows_seen = set()
         self._scal = _Scal()
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
@@ -170,7 +172,7 @@ class CpuSlabTissue(DistributedTissueSolver):
 
     # DevicePcgDriver protocol: the phases gate on the scalar state exactly as
     # pcg_phase_kernel does with a non-null scal
-    def phase_dev(self, kind, mbuf=0):
+    def phase_dev(self, kind, mbuf=0, rows=None, part=None):
         c = self._scal
         if kind in (PH_W0, PH_SWEEP) and c.state != 0:
             return
@@ -178,7 +180,11 @@ class CpuSlabTissue(DistributedTissueSolver):
             return
         if kind == PH_ACT and (c.state in (0, 3) or c.nonfinite != 0.0):
             return
-        self.sums.copy_(self.phase(kind, c.alpha, c.beta, c.first, mbuf))
+        out = self.sums if part is None else self.sum_parts[part]
+        out.copy_(self.phase(kind, c.alpha, c.beta, c.first, mbuf, rows=rows))
+
+    def combine_parts(self, k):
+        torch.sum(self.sum_parts[:k], 0, out=self.sums)
 
     def scalars(self, phase):
         _scalars(self.sums.numpy().copy(), self._scal, phase, self.tol, self.max_iter)
@@ -188,10 +194,16 @@ class CpuSlabTissue(DistributedTissueSolver):
 
         return copy.copy(self._scal)
 
-    def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0):
+    def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0, rows=None):
         o0, o1 = self.o0, self.o1
         A = self.A_loc[self._order]
         di = self.dinv_loc[self._order]
+        if rows is not None:        # the sweep over a sub-range of the owned rows
+            assert kind == PH_SWEEP and self.o0 <= rows[0] < rows[1] <= self.o1
+            o0, o1 = rows
+            A = A[o0 - self.o0:o1 - self.o0]
+            di = di[o0 - self.o0:o1 - self.o0]
+            self.sweep_rows_seen.add((o0, o1))
         x, r, z = self.x.numpy(), self.r.numpy(), self.z_.numpy()
         w, s, p = self.w_.numpy(), self.s_.numpy(), self.p_.numpy()
         out = np.zeros(4)

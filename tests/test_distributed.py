@@ -38,6 +38,27 @@ def test_slab_partition_covers_lattice_once():
         slab_partition((4, 4, 2), 4)
 
 
+def test_sweep_split_rows():
+    """Interior rows never read a ghost plane; interior + boundary = owned."""
+    for lattice, nr in (((40, 14, 6), 2), ((40, 14, 6), 3), ((200, 70, 30), 8),
+                        ((4, 4, 3), 4), ((4, 4, 4), 1)):
+        plane = (lattice[0] + 1) * (lattice[1] + 1)
+        for s in slab_partition(lattice, nr):
+            sp = s.sweep_split()
+            ghosts = [(r0, r1) for _, _, (r0, r1) in s.halo_plan()]
+            if sp is None:
+                assert not ghosts or s.k1 - s.k0 <= len(ghosts)
+                continue
+            (i0, i1), bnd = sp
+            rows = sorted([(i0, i1)] + bnd)
+            assert rows[0][0] == s.own_begin and rows[-1][1] == s.own_end
+            assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+            # the interior's stencil reach (one plane either side) misses the ghosts
+            for g0, g1 in ghosts:
+                assert i1 + plane <= g0 or i0 - plane >= g1
+            assert len(bnd) == len(ghosts)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -70,7 +91,8 @@ def _worker(rank, world, port, steps, out_dir, device_scalars=False):
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u,
                  iters=np.array(solver.iters),
                  act=act[sl.own_begin:sl.own_end],
-                 frozen=frozen[sl.own_begin:sl.own_end])
+                 frozen=frozen[sl.own_begin:sl.own_end],
+                 split_rows=np.array(sorted(solver.sweep_rows_seen)).reshape(-1, 2))
     finally:
         dist.destroy_process_group()
 
@@ -93,6 +115,11 @@ def test_distributed_step_matches_single_domain_oracle(tmp_path, world, device_s
     for r in res:
         np.testing.assert_array_equal(r["u"], res[0]["u"])           # all ranks agree
         np.testing.assert_array_equal(r["iters"], res[0]["iters"])
+    if world == 2:
+        # every rank swept its interior plane during the halo exchange and its
+        # plane next to the ghost after it (distributed.py sweep overlap)
+        for r in res:
+            assert len(r["split_rows"]) == 2, r["split_rows"]
     its = res[0]["iters"]
     assert np.abs(its - np.array(orc.iters)).max() <= 1
     u = res[0]["u"]
