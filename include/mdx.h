@@ -190,6 +190,10 @@ typedef struct mdx_cg_args {
      a_val (the brick-streaming solver passes them as kernel parameters);
      read at launch time only; NULL = use the device table */
   const double* dom_row_host;
+  /* optional HOST copy of the 27 coefficients of class dom_class1 - 1 of
+     m_val (tissue RHS); with dom_row_host it lets the resident solver take
+     both dominant rows as kernel parameters; NULL = fetched from m_val */
+  const double* dom_m_row_host;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */

@@ -72,7 +72,7 @@ class CgArgs(C.Structure):
         ("fail_step", _p), ("variant", _i32), ("dom_class1", _i32),
         ("row_begin", _i64), ("row_end", _i64),
         ("row_out", _p), ("row_probes", _p), ("row_nprobes", _i32), ("_pad2", _i32),
-        ("dom_row_host", _p),
+        ("dom_row_host", _p), ("dom_m_row_host", _p),
     ]
 
 

@@ -519,6 +519,11 @@ class TissueSolver:
             for k, tab in op.host_a.items():
                 self._dom_host[k] = np.ascontiguousarray(tab[a.dom_class1 - 1], np.float64)
         self._dom_ptr = {k: v.ctypes.data for k, v in self._dom_host.items()}
+        # and of M's dominant row (the resident solver's RHS stencil)
+        self._dom_m_host = None
+        if a.dom_class1 > 0 and hasattr(op, "tab_m"):
+            self._dom_m_host = np.ascontiguousarray(op.tab_m[a.dom_class1 - 1], np.float64)
+            a.dom_m_row_host = self._dom_m_host.ctypes.data
         self._dinv_ptr = {k: N.ptr(v) for k, v in op.dinv.items()}
         self._slot_ptr = [N.ptr(self.u_ring[s]) for s in range(RING_SLOTS)]
         self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
