@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define MDX_ABI_VERSION 2
+#define MDX_ABI_VERSION 3
 
 #define MDX_OK 0
 #define MDX_ERR_ARG (-1)

@@ -27,7 +27,7 @@ OP_CSR = 2
 OP_SELL = 3
 ROW_SCRATCH = 1024        # MDX_ROW_SCRATCH
 MAX_LIFT = 8
-ABI_VERSION = 2   # include/mdx.h MDX_ABI_VERSION
+ABI_VERSION = 3   # include/mdx.h MDX_ABI_VERSION
 
 STATUS_DIVERGED = 1
 STATUS_NONFINITE = 2
