@@ -200,7 +200,18 @@ def _sweep_split(be):
     (no neighbours, no interior, or MDX_DIST_OVERLAP=0)."""
     if os.environ.get("MDX_DIST_OVERLAP", "1") == "0":
         return None
-    return be.slab.sweep_split()
+    sp = be.slab.sweep_split()
+    if sp is None:
+        return None
+    # the split costs two more launches per boundary plane and iteration (a
+    # host-enqueue cost): only worth it when the interior sweep is long enough
+    # to hide the exchange - at least MDX_DIST_OVERLAP_MIN (default 4) times
+    # the boundary rows
+    ratio = float(os.environ.get("MDX_DIST_OVERLAP_MIN", "4"))
+    (i0, i1), bnd = sp
+    if i1 - i0 < ratio * sum(b1 - b0 for b0, b1 in bnd):
+        return None
+    return sp
 
 
 class PipelinedPcgDriver:

@@ -73,6 +73,7 @@ def _worker(rank, world, port, steps, out_dir, device_scalars=False):
     sys.path.insert(0, str(Path(__file__).resolve().parent))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["MDX_DIST_OVERLAP_MIN"] = "0"     # exercise the split on the small slab
     import torch.distributed as dist
 
     dist.init_process_group("gloo", rank=rank, world_size=world)

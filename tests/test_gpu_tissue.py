@@ -475,6 +475,7 @@ def _gloo_gpu_worker(rank, world, port, steps, out_dir):
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["MDX_DIST_OVERLAP_MIN"] = "0"     # exercise the halo/interior split
     import torch.distributed as dist
 
     from paper_2308_01651_b200 import configs
