@@ -136,6 +136,7 @@ class SlabComm:
         self.slab = slab
         self.group = group
         self.plan = slab.halo_plan()
+        self.single = dist.get_world_size(group) == 1
 
     def halo(self, *vectors):
         """Fill the ghost planes of each 1-D local vector from the neighbours."""
@@ -181,6 +182,8 @@ class SlabComm:
 
     def allreduce(self, t):
         """Sum a small tensor over ranks in place; returns it."""
+        if self.single:
+            return t
         if t.is_cuda and self.dist.get_backend(self.group) == "gloo":
             h = t.cpu()
             self.dist.all_reduce(h, group=self.group)
@@ -448,12 +451,16 @@ class DistributedTissueSolver:
         return self.ws.z
 
     def _rows_args(self, rows):
-        """The solve's kernel arguments, restricted to local rows [r0, r1)."""
+        """The solve's kernel arguments, restricted to local rows [r0, r1)
+        (one copy per range and step, reused by every iteration)."""
         a = self._args
         if rows is None:
             return a
-        b = N.CgArgs.from_buffer_copy(a)
-        b.row_begin, b.row_end = rows
+        b = self._rows_cache.get(rows)
+        if b is None:
+            b = N.CgArgs.from_buffer_copy(a)
+            b.row_begin, b.row_end = rows
+            self._rows_cache[rows] = b
         return b
 
     def phase(self, kind, alpha=0.0, beta=0.0, first=0, mbuf=0, rows=None):
@@ -570,6 +577,7 @@ class DistributedTissueSolver:
         a.status = N.ptr(self.status)
         a.row_begin, a.row_end = sl.own_begin, sl.own_end
         self._args = a
+        self._rows_cache = {}
 
     def gather_potential(self):
         """Full potential on every rank (all-gather of the owned slabs)."""
