@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define MDX_ABI_VERSION 3
+#define MDX_ABI_VERSION 4
 
 #define MDX_OK 0
 #define MDX_ERR_ARG (-1)
@@ -40,6 +40,15 @@ extern "C" {
 #define MDX_OP_SELL 3      /* SELL-32: rows in chunks of 32, entries column-major per chunk;
                               indptr = chunk offsets (nchunks+1), indices = padded columns,
                               padding entries have value 0 and column = the row itself */
+#define MDX_OP_DIASYM 4    /* symmetric diagonal storage (any mesh whose node numbering puts
+                              most couplings at a few index offsets: structured hex/tet
+                              slabs, the logical-grid ventricle): value block
+                              [1 + dia_np][dia_ld] = diag, then c_s[i] = A[i, i + dia_off[s]]
+                              (0 where absent); A[i, i - d] is read as c_s[i - d].
+                              Couplings at other offsets (the ventricle's periodic seam)
+                              are a row-sorted remainder list, rem_n values appended after
+                              the block, found per 32-row chunk through rem_ptr */
+#define MDX_DIA_MAX 16
 
 #define MDX_MAX_LIFT 8 /* volumes in the ICI lift (simulation.py:342-352) */
 
@@ -127,11 +136,21 @@ typedef struct mdx_operator {
   const int64_t* indptr; /* csr */
   const int32_t* indices;
   int64_t nnz;
+  /* MDX_OP_DIASYM (ABI v4) */
+  int32_t dia_np;        /* positive offsets stored (<= MDX_DIA_MAX) */
+  int32_t _pad1;
+  int64_t dia_ld;        /* stride of the value block (>= n) */
+  int64_t dia_off[MDX_DIA_MAX]; /* ascending positive offsets */
+  int64_t rem_n;         /* remainder entries */
+  const int32_t* rem_ptr;  /* [ceil(n/32) + 1] remainder range of each 32-row chunk */
+  const int32_t* rem_row;  /* [rem_n] row of each remainder entry */
+  const int32_t* rem_col;  /* [rem_n] column of each remainder entry */
 } mdx_operator;
 
 typedef struct mdx_cg_args {
   mdx_operator op;
-  /* operator values: stencil -> [ncls][27] class tables; csr -> [nnz] */
+  /* operator values: stencil -> [ncls][27] class tables; csr -> [nnz];
+     diasym -> [(1 + dia_np) * dia_ld + rem_n] */
   const double* a_val;   /* (alpha/dt) M + K, inactive rows = identity */
   const double* dinv;    /* 1/diag(A): stencil [ncls], csr [n] */
   /* right-hand side: plain solve */

@@ -25,9 +25,11 @@ MODEL_TTP06 = 2
 OP_STENCIL27 = 1
 OP_CSR = 2
 OP_SELL = 3
+OP_DIASYM = 4
+DIA_MAX = 16
 ROW_SCRATCH = 1024        # MDX_ROW_SCRATCH
 MAX_LIFT = 8
-ABI_VERSION = 3   # include/mdx.h MDX_ABI_VERSION
+ABI_VERSION = 4   # include/mdx.h MDX_ABI_VERSION
 
 STATUS_DIVERGED = 1
 STATUS_NONFINITE = 2
@@ -54,6 +56,8 @@ class Operator(C.Structure):
         ("kind", _i32), ("ncls", _i32), ("n", _i64), ("nx1", _i32),
         ("ny1", _i32), ("nz1", _i32), ("_pad", _i32), ("meta", _p),
         ("indptr", _p), ("indices", _p), ("nnz", _i64),
+        ("dia_np", _i32), ("_pad1", _i32), ("dia_ld", _i64), ("dia_off", _i64 * DIA_MAX),
+        ("rem_n", _i64), ("rem_ptr", _p), ("rem_row", _p), ("rem_col", _p),
     ]
 
 

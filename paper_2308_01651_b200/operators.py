@@ -20,6 +20,18 @@ reference's to ~1e-15 relative (`max_rel_dev`).  `CsrOperator` is the
 bit-exact alternative (`TissueSolver(..., operator="csr")`).
 
 `CsrOperator` (any mesh): the reference pattern with device-assembled values.
+
+`DiaOperator` (any mesh whose numbering puts most couplings at a few index
+offsets - every structured slab and the logical-grid ventricle of config 4):
+the CSR values re-laid as symmetric diagonals.  Row i keeps its diagonal and
+its couplings at the positive offsets d_s (c_s[i] = A[i, i + d_s]); the
+coupling A[i, i - d_s] is read from row i - d_s's copy, so a P1-tet row of 15
+entries costs 8 doubles per node and no column indices (120 + 60 B on CSR).
+Couplings at any other offset (the ventricle's periodic seam) stay in a small
+row-sorted remainder list.  The assembled matrices are symmetric up to the
+last bit (the reference sums K_ab and K_ba in different orders): the relative
+deviation introduced by reading the mirror is recorded in `max_rel_dev`
+(~1e-16) and anything above 1e-10 is refused.
 """
 
 import numpy as np
@@ -234,3 +246,116 @@ class CsrOperator:
 
     def device_bytes(self):
         return 12 * self.nnz + 8 * (self.n + 1)
+
+
+class DiaOperator:
+    """Symmetric diagonal layout of a CsrOperator's values (MDX_OP_DIASYM)."""
+
+    kind = N.OP_DIASYM
+    MIN_FRACTION = 0.25           # an offset is stored as a diagonal when this
+    MAX_REMAINDER = 0.05          # fraction of the rows couple there
+
+    @staticmethod
+    def plan(d_indptr, d_indices, n, max_np=N.DIA_MAX):
+        """Diagonal offsets and entry classes of a CSR pattern on the device.
+
+        Returns None when the pattern does not compress (too many offsets or
+        too large a remainder, or an unsymmetric pattern)."""
+        torch = _torch()
+        dev = d_indices.device
+        lens = d_indptr[1:] - d_indptr[:-1]
+        rows = torch.repeat_interleave(torch.arange(n, device=dev), lens)
+        off = d_indices.long() - rows
+        uniq, cnt = torch.unique(off, return_counts=True)
+        cnt_of = dict(zip(uniq.tolist(), cnt.tolist()))
+        cand = [(c, d) for d, c in cnt_of.items()
+                if d > 0 and c >= max(1, int(n * DiaOperator.MIN_FRACTION))]
+        cand.sort(reverse=True)
+        pos = sorted(d for _, d in cand[:max_np])
+        if any(cnt_of.get(-d, 0) != cnt_of[d] for d in pos):
+            return None
+        if not pos:
+            pos = [1]
+        d_pos = torch.tensor(pos, dtype=torch.int64, device=dev)
+        aoff = off.abs()
+        slot = torch.searchsorted(d_pos, aoff).clamp_(max=len(pos) - 1)
+        main = (d_pos[slot] == aoff) & (off != 0)
+        diag = off == 0
+        rem = ~(main | diag)
+        if int(diag.sum()) != n:
+            return None
+        nrem = int(rem.sum())
+        if nrem > DiaOperator.MAX_REMAINDER * off.numel():
+            return None
+        return dict(rows=rows, off=off, slot=slot, upper=main & (off > 0),
+                    lower=main & (off < 0), diag=diag, rem=rem, nrem=nrem, pos=pos)
+
+    def __init__(self, csr, plan):
+        """Convert every value array of `csr` (a CsrOperator built with
+        sell=False) with the plan from `DiaOperator.plan`."""
+        torch = _torch()
+        self.n = n = csr.n
+        self.pos = plan["pos"]
+        self.np_ = len(self.pos)
+        self.ld = ld = ((n + 31) // 32) * 32
+        rows, slot = plan["rows"], plan["slot"]
+        up, lo, dg, rm = plan["upper"], plan["lower"], plan["diag"], plan["rem"]
+        cols = csr.indices.long()
+        self.nrem = plan["nrem"]
+        self._up_idx = (1 + slot[up]) * ld + rows[up]
+        self._lo_mirror = (1 + slot[lo]) * ld + cols[lo]
+        self._dg_idx = rows[dg]
+        self._dg, self._up, self._lo, self._rm = dg, up, lo, rm
+        self.rem_row = rows[rm].to(torch.int32).contiguous()
+        self.rem_col = csr.indices[rm].contiguous()
+        nch = (n + 31) // 32
+        cnt = torch.bincount(rows[rm] >> 5, minlength=nch) if self.nrem else \
+            torch.zeros(nch, dtype=torch.int64, device=rows.device)
+        self.rem_ptr = torch.zeros(nch + 1, dtype=torch.int32, device=rows.device)
+        self.rem_ptr[1:] = torch.cumsum(cnt, 0).to(torch.int32)
+        self.max_rel_dev = 0.0
+        self.a_tables = {k: self._convert(v) for k, v in csr.a_tables.items()}
+        m_new = self._convert(csr.d_m)
+        self.d_lift = [m_new if v is csr.d_m else self._convert(v) for v in csr.d_lift]
+        self.d_m = m_new
+        self.dinv = csr.dinv
+        self.d_inactive, self.d_rest, self.d_thr = csr.d_inactive, csr.d_rest, csr.d_thr
+        self.nnz = csr.nnz
+        del self._up_idx, self._lo_mirror, self._dg_idx, self._dg, self._up, self._lo, self._rm
+        if self.max_rel_dev > 1e-10:
+            raise ValueError(f"operator is not symmetric (relative deviation "
+                             f"{self.max_rel_dev:.3g})")
+
+    def _convert(self, vals):
+        torch = _torch()
+        blk = torch.zeros((1 + self.np_) * self.ld + self.nrem, dtype=torch.float64,
+                          device=vals.device)
+        blk[self._dg_idx] = vals[self._dg]
+        blk[self._up_idx] = vals[self._up]
+        if self.nrem:
+            blk[(1 + self.np_) * self.ld:] = vals[self._rm]
+        lo = vals[self._lo]
+        if lo.numel():
+            mirror = blk[self._lo_mirror]
+            scale = torch.maximum(lo.abs(), mirror.abs()).clamp_min(1e-300)
+            dev = float(((lo - mirror).abs() / scale).max())
+            self.max_rel_dev = max(self.max_rel_dev, dev)
+        return blk
+
+    def operator(self):
+        op = N.Operator()
+        op.kind = N.OP_DIASYM
+        op.n = self.n
+        op.nnz = self.nnz
+        op.dia_np = self.np_
+        op.dia_ld = self.ld
+        for s, d in enumerate(self.pos):
+            op.dia_off[s] = d
+        op.rem_n = self.nrem
+        op.rem_ptr = N.ptr(self.rem_ptr)
+        op.rem_row = N.ptr(self.rem_row)
+        op.rem_col = N.ptr(self.rem_col)
+        return op
+
+    def device_bytes(self):
+        return 8 * (1 + self.np_) * self.ld + 16 * self.nrem

@@ -44,7 +44,7 @@ from .fem import ConductivitySet, DeviceMesh, FeSpace, _sigma_table, detect_latt
 from .geometry import ElementKind, nearest_node
 from .ionic import IonicModelSpec, ModelKind, CellType, pace_single_cell
 from .ionic import model_module
-from .operators import CsrOperator, StencilOperator
+from .operators import CsrOperator, DiaOperator, StencilOperator
 from .outputs import OutputConfig, write_csv, write_vtk
 from .timestepping import ALPHA, bdf_coefficients
 
@@ -297,7 +297,7 @@ def _pad(n):
 class TissueSolver:
     """Owns the device operators and state; advances the coupled system."""
 
-    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=2):
+    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=None):
         validate_config(config)
         self.config = config
         self.timer = SectionTimer()
@@ -306,7 +306,11 @@ class TissueSolver:
         # CG recurrences (csrc/solver.cu): 0 = the reference's verbatim (3 grid
         # syncs per iteration), 1 = q by recurrence (2), 2 = pipelined PCG (1).
         # Same Krylov iterates up to rounding; all checked against the goldens.
-        self.cg_variant = cg_variant
+        # None: pipelined on the SMEM-resident stencil solve (latency-bound),
+        # the reference's recurrences on global-memory operators (bandwidth-
+        # bound: 3 syncs cost nothing there and it moves the fewest vectors).
+        self._cg_variant_req = cg_variant
+        self.cg_variant = 2 if cg_variant is None else cg_variant
         with self.timer.section("Initialization"):
             self._initialize(operator)
 
@@ -386,7 +390,22 @@ class TissueSolver:
                 if operator == "stencil":
                     raise
         if self.op is None:
-            self.op = CsrOperator(dm, self.space, *args, sell=(operator != "csr"))
+            csr = CsrOperator(dm, self.space, *args,
+                              sell=operator not in ("csr", "dia", "auto"))
+            if operator in ("dia", "auto"):
+                plan = DiaOperator.plan(csr.indptr, csr.indices, csr.n)
+                if plan is None and operator == "dia":
+                    raise ValueError("mesh numbering does not compress to diagonals")
+                if plan is not None:
+                    self.op = DiaOperator(csr, plan)
+                    del plan
+                else:
+                    csr._to_sell(*self.space.pattern())
+            if self.op is None:
+                self.op = csr
+            del csr
+            if self._cg_variant_req is None:
+                self.cg_variant = 0
         del K_local, M_local, dm
 
         # device state

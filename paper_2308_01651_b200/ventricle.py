@@ -20,7 +20,7 @@ depth xi in thirds -> materials 1 (endo), 2 (mid), 3 (epi).
 
 import numpy as np
 
-from .geometry import ElementKind, FiberField, KUHN_TETS, Mesh
+from .geometry import ElementKind, FiberField, KUHN_TETS, Mesh, tet_volumes6
 
 INNER_A, INNER_C, WALL = 25e-3, 45e-3, 10e-3
 
@@ -33,32 +33,42 @@ def _coords(xi, th, ph):
 
 
 def prolate_ventricle(n_xi, n_th, n_ph, apex_opening=1e-3):
-    """(mesh, fibers, xi_of_node) for an n_xi x n_th x n_ph logical grid."""
+    """(mesh, fibers, xi_of_node) for an n_xi x n_th x n_ph logical grid.
+
+    Nodes are numbered xi fastest, then th, then ph (node (i_xi, i_th, i_ph) =
+    i_xi + (n_xi+1) (i_th + (n_th+1) i_ph)), cells likewise: every coupling
+    of a node then sits within (n_xi+1)(n_th+2) + 1 indices of it except
+    across the periodic ph seam, which keeps the vectors an operator apply
+    gathers inside a window of a few MB (L2-resident at 10 M nodes).
+    """
     th0 = np.arcsin(apex_opening / INNER_A)
     xi = np.linspace(0.0, 1.0, n_xi + 1)
     th = np.linspace(th0, np.pi / 2, n_th + 1)
     ph = np.arange(n_ph) * (2 * np.pi / n_ph)
-    XI, TH, PH = np.meshgrid(xi, th, ph, indexing="ij")        # node (i_xi, i_th, i_ph)
+    PH, TH, XI = np.meshgrid(ph, th, xi, indexing="ij")        # node (i_ph, i_th, i_xi)
     nodes = _coords(XI, TH, PH).reshape(-1, 3)
+    nx1, nt1 = n_xi + 1, n_th + 1
 
     def nid(i_xi, i_th, i_ph):
-        return (i_ph % n_ph) + n_ph * (i_th + (n_th + 1) * i_xi)
+        return i_xi + nx1 * (i_th + nt1 * (i_ph % n_ph))
 
-    cx, ct, cp = np.meshgrid(np.arange(n_xi), np.arange(n_th), np.arange(n_ph),
-                             indexing="ij")
+    cp, ct, cx = np.meshgrid(np.arange(n_ph, dtype=np.int64), np.arange(n_th, dtype=np.int64),
+                             np.arange(n_xi, dtype=np.int64), indexing="ij")
     cx, ct, cp = cx.ravel(), ct.ravel(), cp.ravel()
     # Kuhn corner q = a + 2b + 4c with offsets (ph: a, th: b, xi: c)
     corner = np.column_stack([nid(cx + ((q >> 2) & 1), ct + ((q >> 1) & 1), cp + (q & 1))
-                              for q in range(8)])
+                              for q in range(8)]).astype(np.int32)
+    del cx, ct, cp
     tets = np.stack([corner[:, list(t)] for t in KUHN_TETS], axis=1).reshape(-1, 4)
+    del corner
     # orient every tet positively
-    e = nodes[tets[:, 1:]] - nodes[tets[:, :1]]
-    det = np.linalg.det(e)
-    flip = det < 0
-    tets[flip] = tets[flip][:, [0, 2, 1, 3]]
-    centroid_xi = XI.reshape(-1)[tets].mean(axis=1)
-    mats = np.where(centroid_xi < 1.0 / 3.0, 1, np.where(centroid_xi < 2.0 / 3.0, 2, 3))
-    mesh = Mesh(nodes, tets.astype(np.int32), ElementKind.TET4, mats.astype(np.int32))
+    flip = np.flatnonzero(tet_volumes6(nodes, tets) < 0)
+    tets[flip, 1], tets[flip, 2] = tets[flip, 2].copy(), tets[flip, 1].copy()
+    # material by centroid depth: the four corners' xi indices
+    xi_idx = (tets % nx1).sum(axis=1)                       # 4 * centroid_xi * n_xi
+    cxi = xi_idx / (4.0 * n_xi)
+    mats = np.where(cxi < 1.0 / 3.0, 1, np.where(cxi < 2.0 / 3.0, 2, 3)).astype(np.int32)
+    mesh = Mesh(nodes, tets, ElementKind.TET4, mats)
 
     # fiber frame from the analytic tangents
     a = INNER_A + WALL * XI

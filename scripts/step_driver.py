@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--h", type=float, default=None)
     ap.add_argument("--operator", default="auto")
     ap.add_argument("--blocks", type=int, default=0)
-    ap.add_argument("--variant", type=int, default=2)
+    ap.add_argument("--variant", type=int, default=None)
     ap.add_argument("--nodes", type=float, default=1e6, help="config 4 target size")
     args = ap.parse_args()
 
@@ -60,7 +60,7 @@ def main():
     wall = time.perf_counter() - t0
     ms = ev[0].elapsed_time(ev[1])
     its = s.iterations_log()[-args.steps:]
-    print(f"n={s.n} op={'stencil' if s.op.kind == 1 else 'csr'} steps={args.steps} "
+    print(f"n={s.n} op={ {1: 'stencil', 2: 'csr', 3: 'sell', 4: 'dia'}[s.op.kind]} variant={s.cg_variant} steps={args.steps} "
           f"device {ms / args.steps:.3f} ms/step host {wall / args.steps * 1e3:.3f} ms/step "
           f"iters {its.min()}..{its.max()} mean {its.mean():.2f} "
           f"DoF*steps/s {s.n * args.steps / (ms * 1e-3):.3e}")

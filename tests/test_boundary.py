@@ -55,7 +55,7 @@ def test_ctypes_binding_covers_header(built):
 
     assert set(header_functions()) == set(_native.EXPORTED_SYMBOLS)
     lib = _native.load_library(built)
-    assert lib.mdx_abi_version() == _native.ABI_VERSION == 3
+    assert lib.mdx_abi_version() == _native.ABI_VERSION == 4
     assert lib.mdx_ionic_num_vars(_native.MODEL_TTP06) == 18
     assert lib.mdx_ionic_num_vars(_native.MODEL_BUENO_OROVIO) == 3
     assert lib.mdx_ionic_num_vars(_native.MODEL_ALIEV_PANFILOV) == 1

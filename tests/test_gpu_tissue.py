@@ -244,11 +244,13 @@ def test_cfg0_csr_path_matches(golden, ns):
     _check(s, pu, g, 5e-5, 300)
 
 
-def test_tet_mesh_run(golden, ns):
+@pytest.mark.parametrize("operator", ["auto", "sell"])
+def test_tet_mesh_run(golden, ns, operator):
     from paper_2308_01651_b200 import configs
 
     g = golden("tissue_tet")
-    s, pu = _run_against(g, configs.config0(ns, kind="Tet4"), 400)
+    s, pu = _run_against(g, configs.config0(ns, kind="Tet4"), 400, operator=operator)
+    assert s.op.kind == {"auto": 4, "sell": 3}[operator]
     _check(s, pu, g, 5e-5, 400)
 
 
@@ -328,6 +330,80 @@ def test_cfg2_full_size_500_steps(golden, ns):
     both = fz & rfz
     act, ref = s.activation_map, g["activation"]
     assert np.abs(act[both] - ref[both]).max() <= dt * (1 + 1e-9)
+
+
+def _run_long(g, cfg, steps, operator="auto"):
+    """Enqueue `steps` steps; the solve writes each step's probe row on the
+    device (no per-step host sync); subsampled snapshots at the golden's
+    stride.  Returns (solver, probe trace, {step: snapshot})."""
+    import torch
+
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    s = TissueSolver(cfg, operator=operator)
+    probes = torch.from_numpy(g["probes"].astype(np.int64)).cuda()
+    rows = torch.zeros((steps, 2 + probes.numel()), dtype=torch.float64, device="cuda")
+    sub = int(g["subsample"])
+    snap_at = sorted(int(k[5:]) for k in g if k.startswith("snap_"))
+    snaps = {}
+    for k in range(steps):
+        s.enqueue_step(record=(probes, rows[k]))
+        if (k + 1) in snap_at:
+            snaps[k + 1] = s.potential_device[::sub].clone()
+        if (k + 1) % 1000 == 0:
+            s.sync()
+    s.sync()
+    return s, rows[:, 2:].cpu().numpy(), {k: v.cpu().numpy() for k, v in snaps.items()}
+
+
+def _check_long(s, pu, snaps, g, steps, dt):
+    """The north_star parity bar on a whole run: CG iterations within +-1 on
+    every step, probe traces and every snapshot within relative L2 1e-6, the
+    same activated set except nodes crossing in the final two steps, and
+    activation times within one dt (goldens store them as step numbers)."""
+    its = s.iterations_log()
+    ref_its = g["iters"][:steps]
+    assert np.abs(its - ref_its).max() <= 1, np.flatnonzero(np.abs(its - ref_its) > 1)[:10]
+    assert _rel(pu, g["probe_u"][:steps]) < 1e-6
+    for k, snap in snaps.items():
+        assert _rel(snap, g[f"snap_{k}"]) < 1e-6, k
+    sub = int(g["subsample"])
+    assert _rel(s.potential[::sub], g["final_u_sub"]) < 1e-6
+    act = s.activation_map
+    ours = np.where(act < 0, -1, np.rint(act / dt)).astype(np.int64)
+    ref = g["activation"].astype(np.int64)
+    on, ron = ours >= 0, ref >= 0
+    late = np.where(on, ours, ref) >= steps - 2
+    assert ((on != ron) & ~late).sum() == 0
+    both = on & ron
+    assert np.abs(ours[both] - ref[both]).max() <= 1
+    return its
+
+
+def test_cfg2_full_run_5000_steps(golden, ns):
+    """Config 2 at its stated size AND length (442,401 nodes, 5,000 steps =
+    100 ms: propagation, plateau, repolarisation) against the reference."""
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg2_full")
+    s, pu, snaps = _run_long(g, configs.config2(ns), 5000)
+    its = _check_long(s, pu, snaps, g, 5000, 2e-5)
+    assert (its == g["iters"]).mean() > 0.95
+    assert (g["activation"] >= 0).all()            # the whole slab activates
+
+
+def test_cfg4_ventricle_100k_60ms(golden, ns):
+    """Config 4 geometry reduced to 128,700 nodes (P1 tets, 3 volumes with
+    duplicated interface states, helix fibers) over 60 ms (3,000 steps), on
+    the diagonal operator, against the reference run on the same mesh."""
+    from paper_2308_01651_b200 import ventricle
+
+    g = golden("tissue_cfg4_100k")
+    cfg = ventricle.config4(ns, *ventricle.size_for_nodes(100_000), final_time=60e-3)
+    s, pu, snaps = _run_long(g, cfg, 3000)
+    assert s.op.kind == 4
+    its = _check_long(s, pu, snaps, g, 3000, 2e-5)
+    assert its.max() >= 20
 
 
 def test_checkpoint_format_and_cross_restore(golden, ns):
@@ -550,10 +626,58 @@ def test_cfg4_ventricle_small(golden, ns):
 
     g = golden("tissue_cfg4_small")
     cfg = config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3)
-    s, pu = _run_against(g, cfg, 1500)
-    assert s.op.kind == 3                                   # SELL-32 (CSR pattern)
-    _check(s, pu, g, 2e-5, 1500)
-    assert _rel(s.potential, g["final_u"]) < 1e-8
+    for operator, kind in (("auto", 4), ("sell", 3)):       # DIASYM, SELL-32
+        s, pu = _run_against(g, cfg, 1500, operator=operator)
+        assert s.op.kind == kind
+        _check(s, pu, g, 2e-5, 1500)
+        assert _rel(s.potential, g["final_u"]) < 1e-8
+
+
+def _spmv(op, vals, x):
+    import torch
+
+    from paper_2308_01651_b200 import _native as N
+
+    a = N.CgArgs()
+    a.op = op.operator()
+    a.a_val = N.ptr(vals)
+    y = torch.empty_like(x)
+    N.check(N.lib().mdx_spmv(N.C.byref(a), N.ptr(x), N.ptr(y), N.stream_handle()))
+    return y.cpu().numpy()
+
+
+def test_dia_operator_matches_csr(ns):
+    """Symmetric diagonal storage (MDX_OP_DIASYM) vs the bit-exact CSR values:
+    A[i, i-d] is read from row i-d's copy, so rows differ from the reference
+    rows by the assembly's own K_ab / K_ba round-off only.  Covers P1 tets
+    (7 stored offsets), the ventricle's periodic seam (remainder list), hex
+    slabs (13 offsets) and the multi-volume lift matrices."""
+    import torch
+
+    from paper_2308_01651_b200 import _native as N, configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+    from paper_2308_01651_b200.ventricle import config4
+
+    cases = [(configs.config0(ns, kind="Tet4"), 8, False),
+             (config4(ns, n_xi=4, n_th=24, n_ph=64), 7, True),
+             (configs.config3(ns, h=0.5e-3), 13, False)]
+    for cfg, nd, seam in cases:
+        dia = TissueSolver(cfg, operator="dia")
+        csr = TissueSolver(cfg, operator="csr")
+        assert dia.op.kind == N.OP_DIASYM and dia.op.np_ <= nd
+        assert (dia.op.nrem > 0) == seam
+        assert dia.op.max_rel_dev < 1e-13
+        x = torch.from_numpy(np.random.default_rng(3).standard_normal(dia.n)).cuda()
+        pairs = [(dia.op.a_tables[k], csr.op.a_tables[k]) for k in dia.op.a_tables]
+        pairs += [(dia.op.d_m, csr.op.d_m)]
+        pairs += list(zip(dia.op.d_lift, csr.op.d_lift))
+        for vd, vc in pairs:
+            yd = _spmv(dia.op, vd, x)
+            yc = _spmv(csr.op, vc, x)
+            scale = _spmv(csr.op, vc.abs(), x.abs())
+            assert (np.abs(yd - yc) <= 1e-13 * scale + 1e-300).all()
+        # device bytes per node: (1 + 7) doubles for tets vs CSR's 12 B/entry
+        assert dia.op.device_bytes() < 0.5 * csr.op.device_bytes()
 
 
 def test_run_loop_rows_csv_and_vtk(golden, ns, tmp_path):

@@ -207,3 +207,67 @@ def test_msh_errors(tmp_path):
     bad.write_text("$Nodes\n1\n1 0 0 0\n$EndNodes\n$Elements\n1\n1 4 1 1 1 2 3 9\n$EndElements\n")
     with pytest.raises(CorruptFile):
         read_msh(bad)
+
+
+def _dia_apply_host(op, blk, x):
+    """numpy restatement of the MDX_OP_DIASYM row (csrc/solver.cu dia_row)."""
+    n, ld = op.n, op.ld
+    b = blk.numpy()
+    y = b[:n] * x
+    for s, d in enumerate(op.pos):
+        c = b[(1 + s) * ld:(1 + s) * ld + n]
+        y[:n - d] += c[:n - d] * x[d:]          # upper: c_s[i] x[i + d]
+        y[d:] += c[:n - d] * x[:n - d]          # lower: c_s[i - d] x[i - d]
+    if op.nrem:
+        rv = b[(1 + op.np_) * ld:]
+        np.add.at(y, op.rem_row.numpy(), rv * x[op.rem_col.numpy()])
+    return y
+
+
+def test_dia_layout_ventricle_seam():
+    """DiaOperator.plan/convert on the host (torch CPU tensors): the 7 Kuhn
+    offsets of the xi-fastest ventricle numbering become diagonals, the
+    periodic ph seam goes to the remainder, and the symmetric apply equals
+    the CSR product."""
+    import types
+
+    import scipy.sparse as sp
+    import torch
+
+    from paper_2308_01651_b200.operators import DiaOperator
+    from paper_2308_01651_b200.ventricle import prolate_ventricle
+
+    n_xi, n_th, n_ph = 3, 6, 40
+    mesh, _, _ = prolate_ventricle(n_xi, n_th, n_ph)
+    n = mesh.num_nodes
+    rng = np.random.default_rng(0)
+    e = mesh.elements
+    rows = np.repeat(e, 4, axis=1).ravel()
+    cols = np.tile(e, (1, 4)).ravel()
+    A = sp.coo_matrix((rng.uniform(0.1, 1.0, rows.size), (rows, cols)), shape=(n, n)).tocsr()
+    A = (A + A.T).tocsr()
+    A.sort_indices()
+    # locality of the numbering: every non-seam coupling within (n_xi+1)(n_th+2)+1
+    coo = A.tocoo()
+    off = np.abs(coo.col - coo.row)
+    seam = off > (n_xi + 1) * (n_th + 2) + 1
+    ph_r = coo.row // ((n_xi + 1) * (n_th + 1))
+    ph_c = coo.col // ((n_xi + 1) * (n_th + 1))
+    assert np.all(np.abs(ph_r - ph_c)[seam] == n_ph - 1)
+    csr = types.SimpleNamespace(
+        n=n, nnz=A.nnz, indices=torch.from_numpy(A.indices.astype(np.int32)),
+        a_tables={2: torch.from_numpy(A.data.copy())}, d_lift=[], dinv={},
+        d_inactive=None, d_rest=None, d_thr=None)
+    csr.d_m = csr.a_tables[2]
+    plan = DiaOperator.plan(torch.from_numpy(A.indptr.astype(np.int64)), csr.indices, n)
+    assert plan is not None
+    op = DiaOperator(csr, plan)
+    assert op.np_ == 7 and op.nrem > 0 and op.max_rel_dev == 0.0
+    x = rng.standard_normal(n)
+    np.testing.assert_allclose(_dia_apply_host(op, op.a_tables[2], x), A @ x, rtol=1e-13)
+    # remainder rows are the two seam planes only, chunk pointers consistent
+    rr = op.rem_row.numpy()
+    assert set(rr // ((n_xi + 1) * (n_th + 1))) == {0, n_ph - 1}
+    ptr = op.rem_ptr.numpy()
+    for c in range(ptr.size - 1):
+        assert np.all(rr[ptr[c]:ptr[c + 1]] // 32 == c)
