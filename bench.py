@@ -1,26 +1,36 @@
-"""Benchmark: monodomain DoF*steps/s of config 2 (BASELINE.json configs[2]).
+"""Benchmark: monodomain DoF*steps/s on config 4 (BASELINE.json configs[4]).
 
 One "step" = one IMEX-BDF2 monodomain time step (TissueSolver.step,
-reference simulation.py:425-483) of the 20x7x3 mm TTP06 slab at h=0.1 mm
-(442,401 nodes): fused ionic update + RHS + Jacobi PCG + activation.
+reference simulation.py:425-483): ionic update (TTP06, three volumes with
+duplicated interface states), ICI right-hand side, Jacobi PCG of
+(alpha/dt M + K) u = b to rtol 1e-10, activation map.
+
+Headline workload: the config-4 ventricle - truncated prolate-spheroid shell,
+P1 tets, 10,276,240 nodes / 59,904,000 tets, helix fibers, endo/mid/epi
+volumes, apical stimulus - the largest BASELINE mesh that fits one GPU.
+The timed window starts at step 500 (t = 10 ms: the activation front is
+travelling through the wall, 61-99 CG iterations per step), reached by
+untimed stepping from rest; W warm-up steps precede it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg4|cfg2]
 
-* ours: warm-up W steps from rest, then K timed steps (the propagation phase:
-  the stimulus fires at t=0, CG needs 7..18 iterations per step).  `value` is
-  device-timed (CUDA events, barrier + synchronize both sides, max over
-  ranks) with all state resident in HBM; `e2e` goes through the public API
-  with host buffers: the initial state is uploaded from a host checkpoint
-  payload in pinned memory (TissueSolver.restore) inside the timed region,
-  and every step
-  reads back the run() output row (t, u_min, u_max, 9 probes) to the host.
-* reference: the reference algorithm on the host CPU cores (oracle port,
-  oracle/, pinned bit-identical to the reference; the reference itself is
-  Python+numba and cannot travel to the GPU box) on a bounded sample of the
-  same workload.
+* ours: `value` is device-timed (CUDA events on the launch stream, barrier +
+  synchronize both sides, max over ranks) with all state resident in HBM;
+  `e2e` goes through the public API with host buffers: the window's start
+  state is uploaded from a checkpoint payload in pinned host memory
+  (TissueSolver.restore) inside the timed region, then the same K steps run
+  and each writes its run() output row (u_min, u_max, 9 probes) into pinned
+  host memory.  `secondary` is config 2 (442,401-node TTP06 slab) from step
+  250 (t = 5 ms, mid-propagation).
+* reference: the reference algorithm on the host CPU cores (oracle port in
+  oracle/, pinned bit-identical to the reference package, which is
+  Python+numba and not installable on the GPU box) on the same mesh: the
+  BDF start-up steps from rest untimed, then K' <= K timed steps (bounded to
+  ~a minute of CPU work).
 
-The ionic state ring (4 x 18 x 442,401 doubles = 255 MB) exceeds the 126 MB
-L2, so no explicit L2 flush is done between steps.
+The ionic state ring (2 x 18 x 10.8 M doubles = 3.1 GB) and the operator
+(6 x 82 MB) exceed the 126 MB L2 many times over: no explicit L2 flush.
 """
 
 import argparse
@@ -28,7 +38,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -37,9 +46,44 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "monodomain DoF*steps/s (config 2: TTP06 slab 442,401 nodes, BDF2, Jacobi PCG)"
 UNIT = "DoF*steps/s"
 FALLBACK_HBM = 6650.0
+
+WORKLOADS = {
+    "cfg4": dict(
+        metric="monodomain DoF*steps/s (config 4: prolate-spheroid ventricle, P1 tets, "
+               "10,276,240 nodes, TTP06 x3 volumes, BDF2, Jacobi PCG)",
+        label="config4 ventricle shell 25/25/45 mm + 10 mm wall, P1 tets (10,276,240 nodes, "
+              "59,904,000 tets), TTP06 endo/mid/epi, BDF2, dt=2e-5 s",
+        window=500, cpu_steps=1),
+    "cfg2": dict(
+        metric="monodomain DoF*steps/s (config 2: TTP06 slab 442,401 nodes, BDF2, Jacobi PCG)",
+        label="config2 TTP06 slab 20x7x3 mm h=0.1 mm (442,401 nodes), BDF2, dt=2e-5 s",
+        window=250, cpu_steps=8),
+}
+
+
+def build_config(name):
+    from paper_2308_01651_b200 import configs
+
+    ns = configs.this_package()
+    if name == "cfg4":
+        from paper_2308_01651_b200 import ventricle
+
+        return ns, ventricle.config4(ns)
+    return ns, configs.config2(ns)
+
+
+def probe_nodes(name, ns, cfg):
+    if name == "cfg4":
+        pts = [(0, 0, -45e-3), (0, 0, -55e-3), (30e-3, 0, 0), (0, 30e-3, 0),
+               (-30e-3, 0, 0), (0, -30e-3, 0), (25e-3, 0, -20e-3), (0, 32e-3, -30e-3),
+               (-27e-3, 0, -10e-3)]
+    else:
+        from paper_2308_01651_b200 import configs
+
+        pts = configs.corner_probes() + [(10e-3, 3.5e-3, 1.5e-3)]
+    return [ns.nearest_node(cfg.mesh, p) for p in pts]
 
 
 def peaks():
@@ -106,7 +150,7 @@ class ClockSampler:
 def traffic_of(kernel):
     """ncu figures of one launch of `kernel` from the committed capture
     (profiles/ncu_traffic.json, written by scripts/summarize_ncu.py):
-    {"dram_bytes", "fp64_flops", ...}, or None."""
+    {"dram_bytes", "fp64_flops", "n", ...}, or None."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         d = json.loads(p.read_text())
@@ -132,251 +176,271 @@ def dist_env():
     return rank, world, local
 
 
-PLATEAU_STEP = 2500          # t = 50 ms at dt = 2e-5 s: every node depolarised
+# ---------------------------------------------------------------------------
+# algorithmic bytes (DESIGN.md section 3 states the per-node
+# figures): fp64, BDF2, fused design
+# ---------------------------------------------------------------------------
 
 
-def cpu_sample(steps, threads=None, warmup=2):
-    """Oracle port of the reference step on cfg 2: `warmup` (>= 2, the BDF
-    start-up) untimed steps from rest, then `steps` timed steps."""
-    if threads:
-        os.environ["OMP_NUM_THREADS"] = str(threads)
+def ionic_bytes(solver):
+    """8 (3 nv + 3) per ionic DOF: read u_n, u_n-1, W_n, W_n-1; write W_n+1, c."""
+    return float(sum(8 * (3 * v.num_vars + 3) * v.dofs.size for v in solver.lift_volumes))
+
+
+def solve_bytes(solver, k):
+    """One solve launch with k CG iterations, per node:
+    RHS: combo 8 + M apply op + per lift volume (I^v 8 + op); r0 = b - A x0:
+    x0 8 + op + r0 8 + D^-1 8; activation 34; reference recurrences 104 + op
+    per iteration; op = bytes of one operator apply per node."""
+    op = solver.op
+    n = solver.n
+    if op.kind == 4:                       # DIASYM: (1 + np) doubles per node
+        opb = 8.0 * (1 + op.np_)
+    elif op.kind == 1:                     # stencil classes: 4-byte node word
+        opb = 4.0
+    else:                                  # CSR / SELL: 12 B per entry
+        opb = 12.0 * op.nnz / n
+    nl = len(solver.lift_volumes)
+    per_iter = 104.0 + opb
+    fixed = 8 + opb + nl * (8 + opb) + 8 + opb + 8 + 8 + 34
+    return n * (fixed + per_iter * np.asarray(k, dtype=np.float64)), opb, per_iter
+
+
+def cpu_sample(name, steps, warmup=2):
+    """Oracle port of the reference step (OpenMP over cells and rows, serial
+    dots like the reference): `warmup` (>= 2, the BDF start-up) untimed steps
+    from rest, then `steps` timed steps on the full mesh."""
     from oracle import monodomain_oracle as O
-    from paper_2308_01651_b200 import configs
 
-    ns = configs.this_package()
-    cfg = configs.config2(ns)
+    ns, cfg = build_config(name)
+    t0 = time.perf_counter()
     orc = O.OracleTissue(cfg)
-    for _ in range(max(2, warmup)):   # BDF1 then BDF2 systems built
+    setup = time.perf_counter() - t0
+    for _ in range(max(2, warmup)):
         orc.step()
     t0 = time.perf_counter()
     for _ in range(steps):
         orc.step()
     wall = time.perf_counter() - t0
     n = cfg.mesh.nodes.shape[0]
-    return n * steps / wall, wall, O.num_threads(), orc.iters[max(2, warmup):]
+    return dict(value=n * steps / wall, wall=wall, cores=O.num_threads(), steps=steps,
+                iters=orc.iters[max(2, warmup):], setup=setup, n=n)
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    # K timed steps of the workload after W warm-up steps, like our arm
-    w = max(2, args.warmup)
-    value, wall, cores, its = cpu_sample(args.steps, warmup=w)
+    w = WORKLOADS[args.workload]
+    steps = max(1, min(args.steps, args.ref_steps or w["cpu_steps"]))
+    r = cpu_sample(args.workload, steps)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": w,
-        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": w["metric"], "value": r["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": 2,
+        "ms_per_step": r["wall"] / steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2 TTP06 slab 20x7x3 mm h=0.1 mm, BDF2, dt=2e-5 s",
-                   "nodes": 442401},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"steps {w + 1}..{w + args.steps} of config 2 from rest "
-                                   f"(CG iterations {min(its)}..{max(its)}), full mesh"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+        "config": {"workload": w["label"], "nodes": r["n"]},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+                         "sample": f"{steps} full step(s) after the 2 BDF start-up steps from "
+                                   f"rest (CG {min(r['iters'])}..{max(r['iters'])}), full mesh, "
+                                   f"oracle setup {r['setup']:.0f} s untimed"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
+def time_window(solver, steps, dist=None, events=True):
+    """K steps device-timed on the launch stream; per-step ionic/solve events."""
     import torch
-
-    from paper_2308_01651_b200 import configs
-    from paper_2308_01651_b200.simulation import TissueSolver
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    # MDX_BENCH_DIST=1: the distributed solver even at one rank (tests the N > 1 path on one GPU)
-    use_dist = world > 1 or os.environ.get("MDX_BENCH_DIST") == "1"
-    if use_dist:
-        import torch.distributed as dist
-
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29541")
-        os.environ.setdefault("RANK", str(rank))
-        os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    ns = configs.this_package()
-    cfg = configs.config2(ns)
-    n = cfg.mesh.nodes.shape[0]
-    if use_dist:
-        return run_distributed(args, cfg, n, rank, world, local, dist)
-    solver = TissueSolver(cfg)
-    init_payload = solver.checkpoint_payload()   # host copy of the initial state
-    for _ in range(args.warmup):
-        solver.enqueue_step()
-    solver.sync()
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-timed region ------------------------------------------------
-    ev_ionic = []
+    per = []
     launches0 = solver.launches
     barrier()
-    with ClockSampler(local) as clocks:
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record()
-        for _ in range(args.steps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e2 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            solver.enqueue_step(events=(e1, e2))
-            ev_ionic.append((e0, e1, e2))
-        end.record()
-        barrier()
-    launches = solver.launches - launches0
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        if events:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            solver.enqueue_step(events=(e[1], e[2]))
+            per.append(e)
+        else:
+            solver.enqueue_step()
+    end.record()
+    barrier()
     ms = start.elapsed_time(end)
-    t = torch.tensor([ms], device="cuda")
     if dist is not None:
+        t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    ionic_ms = np.array([a.elapsed_time(b) for a, b, _ in ev_ionic])
-    solve_ms = np.array([b.elapsed_time(c) for _, b, c in ev_ionic])
-    its = solver.iterations_log()[-args.steps:]
+        ms = float(t.item())
+    its = solver.iterations_log()[-steps:]
+    ionic = np.array([a.elapsed_time(b) for a, b, _ in per]) if per else None
+    solve = np.array([b.elapsed_time(c) for _, b, c in per]) if per else None
+    return ms, its, ionic, solve, solver.launches - launches0
+
+
+def secondary_cfg2(args):
+    """Config 2 from step 250 (mid-propagation), device-timed (beside the headline)."""
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    ns, cfg = build_config("cfg2")
+    s = TissueSolver(cfg)
+    while s.step_index < WORKLOADS["cfg2"]["window"]:
+        s.enqueue_step()
+    s.sync()
+    ms, its, ionic, solve, _ = time_window(s, args.steps)
+    b, _, _ = solve_bytes(s, its)
+    step_b = b + ionic_bytes(s)
+    return {"workload": WORKLOADS["cfg2"]["label"], "from_step": WORKLOADS["cfg2"]["window"],
+            "value": s.n * args.steps / (ms * 1e-3), "unit": UNIT,
+            "ms_per_step": ms / args.steps,
+            "cg_iters_per_step": [int(its.min()), float(its.mean()), int(its.max())],
+            "operator": "stencil27 class tables, SMEM-resident pipelined PCG",
+            "step_frac_hbm": float(step_b.sum() / (ms * 1e-3) / 1e9 / peaks()[0])}
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_distributed(args, rank, world, local, dist)
+
+    wl = WORKLOADS[args.workload]
+    t_setup = time.perf_counter()
+    ns, cfg = build_config(args.workload)
+    n = cfg.mesh.nodes.shape[0]
+    solver = TissueSolver(cfg)
+    setup_s = time.perf_counter() - t_setup
+    for _ in range(args.warmup):
+        solver.enqueue_step()
+    while solver.step_index < max(args.warmup, wl["window"]):
+        solver.enqueue_step()
     solver.sync()
+    window_from = solver.step_index
+    # host copy of the window's start state (the e2e leg's input)
+    payload = solver.checkpoint_payload()
 
-    # ---- plateau phase (reported beside the headline) ------------------------
-    # SURVEY.md 8(d): the propagation phase is CG-bound, the plateau (every node
-    # depolarised, CG 1-2 iterations) ionic/FP64-bound.  The same solver is
-    # advanced untimed to t = 50 ms, then K steps are device-timed again.
-    plateau = None
-    if world == 1 and not args.no_plateau:
-        while solver.step_index < PLATEAU_STEP:
-            solver.enqueue_step()
-        solver.sync()
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        barrier()
-        p0.record()
-        for _ in range(args.steps):
-            solver.enqueue_step()
-        p1.record()
-        barrier()
-        pms = p0.elapsed_time(p1)
-        pits = solver.iterations_log()[-args.steps:]
-        solver.sync()
-        plateau = {"value": n * args.steps / (pms * 1e-3), "unit": UNIT,
-                   "ms_per_step": pms / args.steps, "from_step": PLATEAU_STEP,
-                   "cg_iters_per_step": [int(pits.min()), float(pits.mean()), int(pits.max())],
-                   "bytes_per_step_frac_hbm": float(
-                       n * (562 + 104 * pits.astype(np.float64)).sum()
-                       / (pms * 1e-3) / 1e9 / peaks()[0])}
+    # ---- device-timed region ------------------------------------------------
+    with ClockSampler(local) as clocks:
+        ms, its, ionic_ms, solve_ms, launches = time_window(solver, args.steps)
 
-    # ---- end-to-end through the public API ----------------------------------
-    e2e_solver = TissueSolver(cfg)
-    probes = [ns.nearest_node(cfg.mesh, p) for p in configs.corner_probes()]
-    probes.append(ns.nearest_node(cfg.mesh, (10e-3, 3.5e-3, 1.5e-3)))
+    # ---- end-to-end through the public API (host buffers) -------------------
+    probes = probe_nodes(args.workload, ns, cfg)
     pidx = torch.tensor(probes, device="cuda")
-    e2e_steps = args.steps + args.warmup
-    # the host input: the initial-state checkpoint in pinned memory
-    payload_pinned = torch.frombuffer(bytearray(init_payload), dtype=torch.uint8).pin_memory()
-    pinned = torch.empty((e2e_steps, 2 + len(probes)), dtype=torch.float64, pin_memory=True)
-    barrier()
+    payload_pinned = torch.frombuffer(bytearray(payload), dtype=torch.uint8).pin_memory()
+    del payload
+    rows = torch.empty((args.steps, 2 + len(probes)), dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e2e_solver.restore(payload_pinned)
-    for k in range(e2e_steps):
-        # the run() output row of every step, written by the solve into pinned host memory
-        e2e_solver.enqueue_step(record=(pidx, pinned[k]))
-    e2e_solver.sync()
-    barrier()
-    assert np.isfinite(pinned.numpy()).all()
+    solver.restore(payload_pinned)
+    for k in range(args.steps):
+        solver.enqueue_step(record=(pidx, rows[k]))
+    solver.sync()
     e2e_wall = time.perf_counter() - t0
-    e2e_value = n * e2e_steps * world / e2e_wall
+    e2e_its = solver.iterations_log()[-args.steps:]
+    assert np.isfinite(rows.numpy()).all()
+    e2e = {"value": n * args.steps / e2e_wall, "unit": UNIT,
+           "h2d_bytes_per_step": payload_pinned.numel() / args.steps,
+           "d2h_bytes_per_step": 8 * (2 + len(probes)),
+           "same_steps_as_value": bool(np.array_equal(e2e_its, its))}
 
+    # ---- rooflines ------------------------------------------------------------
     hbm, peak_kind = peaks()
     fp64_peak, fp64_kind = fp64_peak_tflops()
-    nv = 18
-    steps_k = its.astype(np.float64)
-    # SURVEY.md 8(d) algorithmic bytes per node-step (fp64, BDF2, fused design):
-    #   ionic update 8*(3nv+3) = 456 (read u_n, u_n-1, W_n, W_n-1; write W_n+1, c)
-    #   PCG launch: RHS 16 + CG setup 56 + activation 34 + 104 per CG iteration
-    #   whole step 562 + 104 k, k = this step's CG iterations
-    ionic_bytes = n * 8 * (3 * nv + 3)
-    pcg_bytes = n * (16 + 56 + 34 + 104 * steps_k)
-    step_bytes = n * (562 + 104 * steps_k)
-    pcg_share = float(solve_ms.sum() / (ionic_ms.sum() + solve_ms.sum()))
-    ionic_avg = float(ionic_ms.mean()) * 1e-3
-    achieved = ionic_bytes / ionic_avg / 1e9
-    pcg_achieved = float(pcg_bytes.sum() / (solve_ms.sum() * 1e-3) / 1e9)
-    step_achieved = float(step_bytes.sum() / (ms * 1e-3) / 1e9)
-    dominant_pcg = pcg_share > 0.5
-    t_ionic = traffic_of("tissue_ionic")
-    roof_ionic = {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2>",
-                  "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
-                  "unit": "GB/s", "frac": achieved / hbm,
-                  "bytes_per_launch": ionic_bytes,
-                  "traffic": t_ionic.get("dram_bytes") if t_ionic else None}
-    if t_ionic and t_ionic.get("fp64_flops"):
-        # FP64 flops per cell from the ncu SASS counts of one launch (per-cell
-        # constant up to branch divergence), scaled to this launch's n
-        flops = t_ionic["fp64_flops"] / t_ionic.get("n", n) * n
-        roof_ionic["fp64"] = {"achieved": flops / ionic_avg / 1e12, "peak": fp64_peak,
-                              "peak_kind": fp64_kind, "unit": "TFLOP/s",
-                              "frac": flops / ionic_avg / 1e12 / fp64_peak,
-                              "flops_per_launch": flops}
-    t_pcg = traffic_of("pcg_resident_kernel") or traffic_of("pcg_kernel")
-    roof_pcg = {"bound": "hbm", "kernel": "pcg_resident_kernel<tissue,4> (vectors in SMEM: "
-                "HBM roofline of the unfused algorithm's bytes)",
-                "achieved": pcg_achieved, "peak": hbm, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": pcg_achieved / hbm,
-                "bytes_per_launch": float(pcg_bytes.mean()),
-                "traffic": t_pcg.get("dram_bytes") if t_pcg else None}
-    roof_step = {"bound": "hbm", "achieved": step_achieved, "peak": hbm, "unit": "GB/s",
-                 "frac": step_achieved / hbm, "bytes_per_step": float(step_bytes.mean()),
-                 "formula": "n*(562 + 104*k) per step (SURVEY.md 8(d))"}
+    ib = ionic_bytes(solver)
+    sb, opb, per_iter = solve_bytes(solver, its)
+    ionic_s = float(ionic_ms.mean()) * 1e-3
+    solve_share = float(solve_ms.sum() / (ionic_ms.sum() + solve_ms.sum()))
+    pcg_ach = float(sb.sum() / (solve_ms.sum() * 1e-3) / 1e9)
+    ion_ach = ib / ionic_s / 1e9
+    step_ach = float((sb + ib).sum() / (ms * 1e-3) / 1e9)
+    kname = {4: f"pcg_kernel<DIASYM{solver.op.np_},tissue,NPT> (reference CG recurrences)",
+             3: "pcg_kernel<SELL>", 2: "pcg_kernel<CSR>",
+             1: "pcg_resident_kernel<tissue>"}[solver.op.kind]
+    t_pcg = traffic_of("pcg_kernel" if solver.op.kind != 1 else "pcg_resident_kernel")
+    roof_pcg = {"bound": "hbm", "kernel": kname, "achieved": pcg_ach, "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": pcg_ach / hbm,
+                "bytes_per_launch": float(sb.mean()),
+                "bytes_per_node_per_iteration": per_iter,
+                "traffic": (t_pcg.get("dram_bytes") / t_pcg.get("n", n) * n
+                            if t_pcg and t_pcg.get("dram_bytes") else None)}
+    t_ion = traffic_of("tissue_ionic")
+    roof_ion = {"bound": "hbm", "kernel": "tissue_ionic<TTP06,2> (x3 volumes)",
+                "achieved": ion_ach, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": ion_ach / hbm, "bytes_per_step": ib,
+                "traffic": (t_ion.get("dram_bytes") / t_ion.get("n", n) * n
+                            if t_ion and t_ion.get("dram_bytes") else None)}
+    if t_ion and t_ion.get("fp64_flops"):
+        flops = t_ion["fp64_flops"] / t_ion.get("n", n) * ib / 456.0
+        roof_ion["fp64"] = {"achieved": flops / ionic_s / 1e12, "peak": fp64_peak,
+                            "peak_kind": fp64_kind, "unit": "TFLOP/s",
+                            "frac": flops / ionic_s / 1e12 / fp64_peak}
     line = {
-        "metric": METRIC, "value": n * args.steps * world / (ms * 1e-3), "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": wl["metric"], "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2 TTP06 slab 20x7x3 mm h=0.1 mm (442,401 nodes), "
-                               "BDF2, dt=2e-5 s, steps from rest (propagation phase)",
-                   "operator": {1: "stencil27 class tables", 2: "csr", 3: "sell32"}[solver.op.kind],
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "state ring 255 MB > L2; no flush",
-                   "cg_iters_per_step": [int(its.min()), float(its.mean()), int(its.max())]},
+        "config": {"workload": wl["label"], "nodes": n,
+                   "window": f"steps {window_from + 1}..{window_from + args.steps} "
+                             f"(t = {window_from * cfg.dt * 1e3:.1f} ms on, propagation)",
+                   "operator": {1: "stencil27 class tables", 2: "csr", 3: "sell32",
+                                4: f"diasym ({solver.op.np_} offsets, "
+                                   f"{solver.op.nrem} seam entries)"}[solver.op.kind],
+                   "cg_variant": solver.cg_variant,
+                   "parallelism": "single",
+                   "l2": "state 3 GB and operator 0.5 GB >> 126 MB L2; no flush",
+                   "cg_iters_per_step": [int(its.min()), float(its.mean()), int(its.max())],
+                   "setup_s": setup_s},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
         "kernels": {"ionic_ms": float(ionic_ms.mean()), "pcg_ms": float(solve_ms.mean()),
-                    "pcg_share": pcg_share},
-        "roofline": roof_pcg if dominant_pcg else roof_ionic,
-        "roofline_other": roof_ionic if dominant_pcg else roof_pcg,
-        "roofline_step": roof_step,
-        "phases": {"propagation": {"value": n * args.steps * world / (ms * 1e-3),
-                                   "from_step": args.warmup},
-                   "plateau": plateau},
-        "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": len(init_payload) / e2e_steps,
-                "d2h_bytes_per_step": 8 * (2 + len(probes))},
+                    "pcg_share": solve_share},
+        "roofline": roof_pcg if solve_share > 0.5 else roof_ion,
+        "roofline_other": roof_ion if solve_share > 0.5 else roof_pcg,
+        "roofline_step": {"bound": "hbm", "achieved": step_ach, "peak": hbm, "unit": "GB/s",
+                          "frac": step_ach / hbm, "bytes_per_step": float((sb + ib).mean())},
+        "e2e": e2e,
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        value, wall, cores, cits = cpu_sample(args.cpu_steps)
+    del solver, payload_pinned
+    torch.cuda.empty_cache()
+    if args.workload == "cfg4" and not args.no_secondary:
+        line["secondary"] = secondary_cfg2(args)
+    if not args.no_cpu:
+        r = cpu_sample(args.workload, args.cpu_steps or wl["cpu_steps"])
         line["cpu_baseline"] = {
-            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle port, steps 3..{2 + args.cpu_steps} of config 2 from rest"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+            "value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+            "sample": f"oracle port, {r['steps']} full step(s) of the same mesh after the 2 "
+                      f"BDF start-up steps from rest (CG {min(r['iters'])}..{max(r['iters'])})"}
+    print(json.dumps(line), flush=True)
 
 
-def run_distributed(args, cfg, n, rank, world, local, dist):
-    """N > 1: config 2 split over the ranks (z-slabs, NCCL halo + all-reduce),
+def run_distributed(args, rank, world, local, dist):
+    """N > 1: the mesh partitioned over the ranks (paper_2308_01651_b200.distributed),
     strong scaling (total work fixed)."""
     import torch
 
     from paper_2308_01651_b200.distributed import DistributedTissueSolver
 
+    wl = WORKLOADS[args.workload]
+    ns, cfg = build_config(args.workload)
+    n = cfg.mesh.nodes.shape[0]
     solver = DistributedTissueSolver(cfg)
-    for _ in range(args.warmup):
+    while solver.step_index < max(args.warmup, wl["window"]):
         solver.step()
     dist.barrier()
     torch.cuda.synchronize()
@@ -396,63 +460,66 @@ def run_distributed(args, cfg, n, rank, world, local, dist):
     its = np.array(solver.iters[-args.steps:])
     launches = solver.launches - launches0
 
-    # ---- e2e: every rank re-uploads its slab state (rings, activation) from
-    # pinned host memory, then runs the same K steps through the public
-    # step() and reads each step's local potential range back to the host
-    names = ("u_ring", "w_ring", "act_time", "best_slope", "frozen")
-    snap = {k: getattr(solver, k).cpu().pin_memory() for k in names}
-    head, step_index, time_s = solver.head, solver.step_index, solver.time
-    h2d = sum(v.numel() * v.element_size() for v in snap.values())
-    sl = solver.slab
+    # e2e: every rank re-uploads its window-start state from pinned host
+    # memory, runs the same K steps through step() and reads each step's
+    # local potential range back to the host
+    snap = solver.snapshot_host()
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in names:
-        getattr(solver, k).copy_(snap[k], non_blocking=True)
-    solver.head, solver.step_index, solver.time = head, step_index, time_s
+    h2d = solver.restore_host(snap)
     for _ in range(args.steps):
         solver.step()
-        u = solver.potential_local()[sl.own_begin:sl.own_end]
-        torch.stack([u.min(), u.max()]).cpu()
+        solver.local_range().cpu()
     dist.barrier()
     torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
     dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-    e2e = {"value": n * args.steps / float(wall.item()), "unit": UNIT,
-           "h2d_bytes_per_step": h2d * world / args.steps, "d2h_bytes_per_step": 16 * world}
     if rank == 0:
         line = {
-            "metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
+            "metric": wl["metric"], "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2 TTP06 slab 442,401 nodes, BDF2, dt=2e-5 s",
-                       "parallelism": f"z-slab domain decomposition x{world}, NCCL halo + "
-                                      "all-reduce, pipelined PCG with device-resident scalars, "
-                                      "halo overlapped with the interior-plane sweep",
+            "config": {"workload": wl["label"], "nodes": n,
+                       "parallelism": solver.describe(),
                        "cg_iters_per_step": [int(its.min()), float(its.mean()),
                                              int(its.max())]},
             "clocks": clocks.summary(),
             "gpu_launches": launches,
-            "e2e": e2e,
+            "e2e": {"value": n * args.steps / float(wall.item()), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d * world / args.steps,
+                    "d2h_bytes_per_step": 16 * world},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
 
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29500 + os.getpid() % 1000), str(ROOT / "bench.py")]
+    cmd += [a for a in sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--no-plateau", action="store_true",
-                    help="skip the plateau-phase sample (t = 50 ms) of the same run")
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--cpu-steps", type=int, default=0)
+    ap.add_argument("--ref-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

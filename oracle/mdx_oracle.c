@@ -423,6 +423,181 @@ void orc_assemble_stiffness(long ne, int nl, int nq, const double* nodes, const 
   }
 }
 
+/* ------------------------------------------------------------------ */
+/* Large meshes (config 4, 10 M nodes): the same pattern and the same   */
+/* element-order sums, built in parallel.                               */
+/* ------------------------------------------------------------------ */
+#include <stdlib.h>
+
+/* node -> incident elements, ascending (counting sort by node) */
+void orc_incidence(long n, long ne, int nl, const int32_t* elems, int64_t* ptr, int32_t* elem) {
+  memset(ptr, 0, sizeof(int64_t) * (n + 1));
+  for (long k = 0; k < ne * nl; ++k) ptr[elems[k] + 1]++;
+  for (long i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
+  int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * n);
+  memcpy(cur, ptr, sizeof(int64_t) * n);
+  for (long e = 0; e < ne; ++e)
+    for (int a = 0; a < nl; ++a) elem[cur[elems[e * nl + a]]++] = (int32_t)e;
+  free(cur);
+}
+
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* sorted unique neighbours of row i into buf; returns the count */
+static int row_cols(long i, int nl, const int32_t* elems, const int64_t* ptr,
+                    const int32_t* elem, int32_t* buf) {
+  int m = 0;
+  for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k)
+    for (int a = 0; a < nl; ++a) buf[m++] = elems[(long)elem[k] * nl + a];
+  qsort(buf, m, sizeof(int32_t), cmp_i32);
+  int u = 0;
+  for (int k = 0; k < m; ++k)
+    if (u == 0 || buf[k] != buf[u - 1]) buf[u++] = buf[k];
+  return u;
+}
+
+/* FeSpace pattern (all node pairs sharing an element, rows sorted):
+ * pass 1 (indices == NULL) fills indptr, pass 2 the column indices */
+void orc_pattern_rows(long n, int nl, const int32_t* elems, const int64_t* ptr,
+                      const int32_t* elem, int64_t* indptr, int32_t* indices) {
+  long maxdeg = 0;
+  for (long i = 0; i < n; ++i)
+    if (ptr[i + 1] - ptr[i] > maxdeg) maxdeg = ptr[i + 1] - ptr[i];
+  if (!indices) indptr[0] = 0;
+#pragma omp parallel
+  {
+    int32_t* buf = (int32_t*)malloc(sizeof(int32_t) * (maxdeg * nl + 1));
+#pragma omp for schedule(static)
+    for (long i = 0; i < n; ++i) {
+      int u = row_cols(i, nl, elems, ptr, elem, buf);
+      if (!indices) indptr[i + 1] = u;
+      else memcpy(indices + indptr[i], buf, sizeof(int32_t) * u);
+    }
+    free(buf);
+  }
+  if (!indices)
+    for (long i = 0; i < n; ++i) indptr[i + 1] += indptr[i];
+}
+
+/* Element matrices of [e0, e1) in parallel (the per-element arithmetic of
+ * orc_assemble_mass / orc_assemble_stiffness), then the scatter row by row:
+ * each row adds its incident elements' entries in ascending element order,
+ * exactly the order of the serial element loop, so the sums are identical. */
+static void local_mass(const double* nodes, const int32_t* conn, int nl, int nq,
+                       const double* w, const double* basis, const double* grad, double* out) {
+  double jac[3][3];
+  for (int k = 0; k < nl * nl; ++k) out[k] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double det = jac_det(nodes, conn, nl, grad + q * nl * 3, jac);
+    double scale = w[q] * det;
+    for (int a = 0; a < nl; ++a) {
+      double va = basis[q * nl + a] * scale;
+      for (int b = 0; b < nl; ++b) out[a * nl + b] += va * basis[q * nl + b];
+    }
+  }
+}
+
+static void local_stiff(const double* nodes, const int32_t* conn, int nl, int nq,
+                        double sl, double st, double sn, const double* f0, const double* s0,
+                        const double* w, const double* basis, const double* grad, double* out) {
+  double jac[3][3], inv[3][3], g[8][3], T[3][3];
+  for (int k = 0; k < nl * nl; ++k) out[k] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    const double* gq = grad + q * nl * 3;
+    double det = jac_det(nodes, conn, nl, gq, jac);
+    double id = 1.0 / det;
+    inv[0][0] = (jac[1][1] * jac[2][2] - jac[1][2] * jac[2][1]) * id;
+    inv[0][1] = (jac[0][2] * jac[2][1] - jac[0][1] * jac[2][2]) * id;
+    inv[0][2] = (jac[0][1] * jac[1][2] - jac[0][2] * jac[1][1]) * id;
+    inv[1][0] = (jac[1][2] * jac[2][0] - jac[1][0] * jac[2][2]) * id;
+    inv[1][1] = (jac[0][0] * jac[2][2] - jac[0][2] * jac[2][0]) * id;
+    inv[1][2] = (jac[0][2] * jac[1][0] - jac[0][0] * jac[1][2]) * id;
+    inv[2][0] = (jac[1][0] * jac[2][1] - jac[1][1] * jac[2][0]) * id;
+    inv[2][1] = (jac[0][1] * jac[2][0] - jac[0][0] * jac[2][1]) * id;
+    inv[2][2] = (jac[0][0] * jac[1][1] - jac[0][1] * jac[1][0]) * id;
+    for (int a = 0; a < nl; ++a)
+      for (int i = 0; i < 3; ++i)
+        g[a][i] = inv[0][i] * gq[a * 3] + inv[1][i] * gq[a * 3 + 1] + inv[2][i] * gq[a * 3 + 2];
+    double fq[3] = {0, 0, 0}, sq[3] = {0, 0, 0}, nq3[3];
+    for (int a = 0; a < nl; ++a) {
+      double wa = basis[q * nl + a];
+      for (int i = 0; i < 3; ++i) {
+        fq[i] += wa * f0[conn[a] * 3 + i];
+        sq[i] += wa * s0[conn[a] * 3 + i];
+      }
+    }
+    double fnrm = sqrt(fq[0] * fq[0] + fq[1] * fq[1] + fq[2] * fq[2]);
+    for (int i = 0; i < 3; ++i) fq[i] /= fnrm;
+    double d = fq[0] * sq[0] + fq[1] * sq[1] + fq[2] * sq[2];
+    for (int i = 0; i < 3; ++i) sq[i] -= d * fq[i];
+    double snrm = sqrt(sq[0] * sq[0] + sq[1] * sq[1] + sq[2] * sq[2]);
+    for (int i = 0; i < 3; ++i) sq[i] /= snrm;
+    nq3[0] = fq[1] * sq[2] - fq[2] * sq[1];
+    nq3[1] = fq[2] * sq[0] - fq[0] * sq[2];
+    nq3[2] = fq[0] * sq[1] - fq[1] * sq[0];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        T[i][j] = sl * fq[i] * fq[j] + st * sq[i] * sq[j] + sn * nq3[i] * nq3[j];
+    double scale = w[q] * det;
+    for (int a = 0; a < nl; ++a) {
+      double d0 = T[0][0] * g[a][0] + T[0][1] * g[a][1] + T[0][2] * g[a][2];
+      double d1 = T[1][0] * g[a][0] + T[1][1] * g[a][1] + T[1][2] * g[a][2];
+      double d2 = T[2][0] * g[a][0] + T[2][1] * g[a][1] + T[2][2] * g[a][2];
+      for (int b = 0; b < nl; ++b)
+        out[a * nl + b] += scale * (d0 * g[b][0] + d1 * g[b][1] + d2 * g[b][2]);
+    }
+  }
+}
+
+/* kind 0: mass over elements with include[e]; kind 1: stiffness over
+ * elements with sigma_rows[e] >= 0.  ptr/elem: orc_incidence. */
+void orc_assemble_par(int kind, long n, long ne, int nl, int nq, const double* nodes,
+                      const int32_t* elems, const uint8_t* include, const int64_t* sigma_rows,
+                      const double* sigmas, const double* f0, const double* s0, const double* w,
+                      const double* basis, const double* grad, const int64_t* indptr,
+                      const int32_t* indices, const int64_t* ptr, const int32_t* elem,
+                      double* data) {
+  const long chunk = 1L << 21;
+  double* loc = (double*)malloc(sizeof(double) * chunk * nl * nl);
+  int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * n);
+  memcpy(cur, ptr, sizeof(int64_t) * n);
+  for (long e0 = 0; e0 < ne; e0 += chunk) {
+    const long e1 = e0 + chunk < ne ? e0 + chunk : ne;
+#pragma omp parallel for schedule(static)
+    for (long e = e0; e < e1; ++e) {
+      double* out = loc + (e - e0) * nl * nl;
+      const int32_t* conn = elems + e * nl;
+      if (kind == 0) {
+        if (include[e]) local_mass(nodes, conn, nl, nq, w, basis, grad, out);
+      } else {
+        long sr = sigma_rows[e];
+        if (sr >= 0)
+          local_stiff(nodes, conn, nl, nq, sigmas[sr * 3], sigmas[sr * 3 + 1],
+                      sigmas[sr * 3 + 2], f0, s0, w, basis, grad, out);
+      }
+    }
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) {
+      int64_t k = cur[i];
+      for (; k < ptr[i + 1] && elem[k] < e1; ++k) {
+        const long e = elem[k];
+        if (kind == 0 ? !include[e] : sigma_rows[e] < 0) continue;
+        const int32_t* conn = elems + e * nl;
+        int a = 0;
+        while (conn[a] != i) ++a;
+        const double* row = loc + (e - e0) * nl * nl + a * nl;
+        for (int b = 0; b < nl; ++b) csr_add(indptr, indices, data, i, conn[b], row[b]);
+      }
+      cur[i] = k;
+    }
+  }
+  free(cur);
+  free(loc);
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   extern int omp_get_max_threads(void);

@@ -62,6 +62,10 @@ def lib():
         _lib.orc_assemble_stiffness.argtypes = [C.c_long, C.c_int, C.c_int, P, P, P, P,
                                                 P, P, P, P, P, P, P, P]
         _lib.orc_num_threads.restype = C.c_int
+        _lib.orc_incidence.argtypes = [C.c_long, C.c_long, C.c_int, P, P, P]
+        _lib.orc_pattern_rows.argtypes = [C.c_long, C.c_int, P, P, P, P, P]
+        _lib.orc_assemble_par.argtypes = [C.c_int, C.c_long, C.c_long, C.c_int, C.c_int,
+                                          P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
     return _lib
 
 
@@ -166,42 +170,62 @@ def _tables(kind):
     return np.full(4, 1.0 / 24.0), vals, np.broadcast_to(g, (4, 4, 3)).copy()
 
 
+class Pattern(tuple):
+    """(indptr, indices) of FeSpace.pattern (fem.py:242-259) plus the node ->
+    incident-element lists the parallel assembly walks."""
+
+    incidence = None
+
+
 def pattern(n, elements):
-    e = np.asarray(elements, np.int64)
-    nl = e.shape[1]
-    keys = np.unique((np.repeat(e, nl, axis=1) * n + np.tile(e, (1, nl))).ravel())
-    rows = keys // n
-    indptr = np.zeros(n + 1, np.int64)
-    np.cumsum(np.bincount(rows, minlength=n), out=indptr[1:])
-    return indptr, (keys % n).astype(np.int32)
+    """Sorted unique node pairs sharing an element, rows in parallel (C)."""
+    el = np.ascontiguousarray(elements, np.int32)
+    ne, nl = el.shape
+    ptr = np.empty(n + 1, np.int64)
+    elem = np.empty(ne * nl, np.int32)
+    lib().orc_incidence(n, ne, nl, _p(el), _p(ptr), _p(elem))
+    indptr = np.empty(n + 1, np.int64)
+    lib().orc_pattern_rows(n, nl, _p(el), _p(ptr), _p(elem), _p(indptr), None)
+    indices = np.empty(int(indptr[-1]), np.int32)
+    lib().orc_pattern_rows(n, nl, _p(el), _p(ptr), _p(elem), _p(indptr), _p(indices))
+    pat = Pattern((indptr, indices))
+    pat.incidence = (ptr, elem)
+    return pat
+
+
+def _assemble(kind, mesh, pat, include=None, sigma_rows=None, sigmas=None, fibers=None):
+    """Element-order sums of fem.py:280-426, element matrices in parallel and
+    each row scattered in ascending element order (identical sums)."""
+    w, basis, grad = _tables(mesh.element_kind.value)
+    indptr, indices = pat
+    ptr, elem = pat.incidence
+    data = np.zeros(indices.size)
+    nodes = np.ascontiguousarray(mesh.nodes, np.float64)
+    el = np.ascontiguousarray(mesh.elements, np.int32)
+    inc = sr = sg = f0 = s0 = None
+    if kind == 0:
+        inc = np.ascontiguousarray(include, np.uint8)
+    else:
+        sr = np.ascontiguousarray(sigma_rows, np.int64)
+        sg = np.ascontiguousarray(np.asarray(sigmas, np.float64).reshape(-1, 3))
+        f0 = np.ascontiguousarray(fibers.f0, np.float64)
+        s0 = np.ascontiguousarray(fibers.s0, np.float64)
+
+    def pp(a):
+        return None if a is None else _p(a)
+
+    lib().orc_assemble_par(kind, nodes.shape[0], el.shape[0], el.shape[1], w.size, _p(nodes),
+                           _p(el), pp(inc), pp(sr), pp(sg), pp(f0), pp(s0), _p(w), _p(basis),
+                           _p(grad), _p(indptr), _p(indices), _p(ptr), _p(elem), _p(data))
+    return Csr(indptr, indices, data)
 
 
 def assemble_mass(mesh, include, pat):
-    w, basis, grad = _tables(mesh.element_kind.value)
-    indptr, indices = pat
-    data = np.zeros(indices.size)
-    nodes = np.ascontiguousarray(mesh.nodes, np.float64)
-    el = np.ascontiguousarray(mesh.elements, np.int32)
-    inc = np.ascontiguousarray(include, np.uint8)
-    lib().orc_assemble_mass(el.shape[0], el.shape[1], w.size, _p(nodes), _p(el), _p(inc),
-                            _p(w), _p(basis), _p(grad), _p(indptr), _p(indices), _p(data))
-    return Csr(indptr, indices, data)
+    return _assemble(0, mesh, pat, include=include)
 
 
 def assemble_stiffness(mesh, sigma_rows, sigmas, fibers, pat):
-    w, basis, grad = _tables(mesh.element_kind.value)
-    indptr, indices = pat
-    data = np.zeros(indices.size)
-    nodes = np.ascontiguousarray(mesh.nodes, np.float64)
-    el = np.ascontiguousarray(mesh.elements, np.int32)
-    sr = np.ascontiguousarray(sigma_rows, np.int64)
-    sg = np.ascontiguousarray(np.asarray(sigmas, np.float64).reshape(-1, 3))
-    f0 = np.ascontiguousarray(fibers.f0, np.float64)
-    s0 = np.ascontiguousarray(fibers.s0, np.float64)
-    lib().orc_assemble_stiffness(el.shape[0], el.shape[1], w.size, _p(nodes), _p(el),
-                                 _p(sr), _p(sg), _p(f0), _p(s0), _p(w), _p(basis),
-                                 _p(grad), _p(indptr), _p(indices), _p(data))
-    return Csr(indptr, indices, data)
+    return _assemble(1, mesh, pat, sigma_rows=sigma_rows, sigmas=sigmas, fibers=fibers)
 
 
 def add_scaled(c, M, K):

@@ -1,6 +1,10 @@
 """Summarise ncu reports (.ncu-rep) and a launch-list CSV into profiles/.
 
     python scripts/summarize_ncu.py <out.md> <launches.csv> <rep1> [<rep2> ...]
+                                    [--n KERNEL_SUBSTRING=ROWS ...]
+
+--n records how many nodes/DOFs the captured launch processed, so bench.py can
+scale the per-launch DRAM bytes to its own launch size.
 """
 import csv
 import io
@@ -29,8 +33,13 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """(metrics, kernel name) of a .ncu-rep, or of its `--page raw --csv`
+    export (a *_raw.csv file written on the GPU box)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}, vals[hdr.index("Kernel Name")]
@@ -38,9 +47,16 @@ def raw(rep):
 
 def fp64_flops(rep):
     """FP64 flops of the captured launch from the SASS source page
-    (thread-level executed DFMA x2 + DMUL + DADD)."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    (thread-level executed DFMA x2 + DMUL + DADD); for a *_raw.csv export the
+    matching *_sass.csv next to it."""
+    if rep.endswith("_raw.csv"):
+        try:
+            out = open(rep[:-len("_raw.csv")] + "_sass.csv").read()
+        except OSError:
+            return None
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                              "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3 or "Source" not in rows[1]:
         return None
@@ -81,7 +97,14 @@ def main():
     import json
     from pathlib import Path
 
-    out, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    argv = sys.argv[1:]
+    sizes = {}
+    while "--n" in argv:
+        i = argv.index("--n")
+        k, v = argv[i + 1].split("=")
+        sizes[k] = int(float(v))
+        del argv[i:i + 2]
+    out, launches, reps = argv[0], argv[1], argv[2:]
     lines = ["# ncu summary", ""]
     traffic = {}
     for rep in reps:
@@ -96,6 +119,9 @@ def main():
             fl = fp64_flops(rep)
             if fl:
                 entry["fp64_flops"] = fl
+            for k, v in sizes.items():
+                if k in name:
+                    entry["n"] = v
             traffic[name.split("(")[0]] = entry
         except (KeyError, ValueError):
             pass
@@ -108,7 +134,8 @@ def main():
         lines += ["", "top stall reasons (warps per issued instruction): " +
                   ", ".join(f"{n} {v:.2f}" for v, n in stalls(d)), ""]
     # launch list: share of device time per kernel
-    rows = list(csv.DictReader(l for l in open(launches) if not l.startswith("==")))
+    rows = ([] if launches == "-" else
+            list(csv.DictReader(l for l in open(launches) if not l.startswith("=="))))
     tot = defaultdict(float)
     cnt = defaultdict(int)
     for r in rows:
@@ -119,7 +146,7 @@ def main():
         scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r["Metric Unit"], 1.0)
         tot[k] += v * scale
         cnt[k] += 1
-    all_t = sum(tot.values())
+    all_t = sum(tot.values()) or 1.0
     lines += ["## launch list (ncu, --clock-control none, serialised, cold cache)", "",
               "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
