@@ -213,6 +213,13 @@ typedef struct mdx_cg_args {
      m_val (tissue RHS); with dom_row_host it lets the resident solver take
      both dominant rows as kernel parameters; NULL = fetched from m_val */
   const double* dom_m_row_host;
+  /* distributed phases (ABI v4): when row_mask is set, mdx_pcg_phase[_dev]
+     processes (and sums) only the rows i of [row_begin, row_end) with
+     row_mask[i] & row_select != 0 (1 = owned interior, 2 = owned next to a
+     ghost, 0 = ghost); NULL = every row of the range */
+  const uint8_t* row_mask;
+  int32_t row_select;
+  int32_t _pad3;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */
@@ -247,6 +254,10 @@ int mdx_pcg_scalars(const double* sums, mdx_pcg_scal* scal, int phase, double to
  * for a zero right-hand side, activation only after a finite solve). */
 int mdx_pcg_phase_dev(const mdx_cg_args* args, int phase, int tissue, const mdx_pcg_scal* scal,
                       int mbuf, double* sums_out, void* stream);
+/* Halo packing of the distributed solver: dst[k] = src[idx[k]] (gather)
+   and dst[idx[k]] = src[k] (scatter), k < n */
+int mdx_gather(int64_t n, const int64_t* idx, const double* src, double* dst, void* stream);
+int mdx_scatter(int64_t n, const int64_t* idx, const double* src, double* dst, void* stream);
 /* y = A x with the same row arithmetic (csr_matvec, linalg.py:17-23) */
 int mdx_spmv(const mdx_cg_args* args, const double* x, double* y, void* stream);
 

@@ -77,6 +77,7 @@ class CgArgs(C.Structure):
         ("row_begin", _i64), ("row_end", _i64),
         ("row_out", _p), ("row_probes", _p), ("row_nprobes", _i32), ("_pad2", _i32),
         ("dom_row_host", _p), ("dom_m_row_host", _p),
+        ("row_mask", _p), ("row_select", _i32), ("_pad3", _i32),
     ]
 
 
@@ -132,6 +133,8 @@ _SIGNATURES = {
                           C.c_int),
     "mdx_pcg_scalars": ([_p, _p, C.c_int, _d, C.c_int, _p], C.c_int),
     "mdx_spmv": ([C.POINTER(CgArgs), _p, _p, _p], C.c_int),
+    "mdx_gather": ([_i64, _p, _p, _p, _p], C.c_int),
+    "mdx_scatter": ([_i64, _p, _p, _p, _p], C.c_int),
     "mdx_assemble_local": ([C.POINTER(AssemblyArgs), _p], C.c_int),
     "mdx_scatter_csr": ([_i64, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
                         C.c_int),

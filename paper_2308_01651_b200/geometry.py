@@ -100,6 +100,9 @@ class Mesh:
     element_kind: ElementKind
     material_ids: np.ndarray
     lattice: tuple = field(default=None, compare=False)
+    # logical node grid ((d0, d1, d2), (periodic0, periodic1, periodic2)) with
+    # node id = i0 + d0 (i1 + d1 i2), when the generator knows it (ventricle)
+    grid: tuple = field(default=None, compare=False)
 
     def __post_init__(self):
         self.nodes = np.ascontiguousarray(self.nodes, dtype=np.float64)
@@ -138,7 +141,7 @@ class Mesh:
     def with_materials(self, material_ids):
         """Same geometry and lattice, new per-element material IDs."""
         return Mesh(self.nodes, self.elements, self.element_kind,
-                    material_ids, lattice=self.lattice)
+                    material_ids, lattice=self.lattice, grid=self.grid)
 
 
 @dataclass(frozen=True)

@@ -547,29 +547,20 @@ class TissueSolver:
         self._slot_ptr = [N.ptr(self.u_ring[s]) for s in range(RING_SLOTS)]
         self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
 
-    def enqueue_step(self, events=None, record=None):
-        """Launch one step; no host synchronisation.
-
-        `events`: optional (after_ionic, after_solve) CUDA events recorded on
-        the launch stream (bench.py's per-kernel timing).
-        `record`: optional (probe_idx, dst): the solve itself writes the run()
-        output row [u_min, u_max, u[probes]] of the new potential into `dst`
-        (a pinned host float64 row, written through its device mapping, or a
-        CUDA tensor) - no extra kernel or copy.
-        """
-        import torch
-
+    def step_plan(self):
+        """(order, t_next, active-impulse mask, head slot, next slot) of the
+        next step (simulation.py:427-431)."""
         order = min(self.step_index + 1, self.config.bdf_order)
         t_next = self.time + self.dt
         mask = self._active_mask(t_next) if self._impulses else 0
+        head = self.head
+        return order, t_next, mask, head, (head + 1) % RING_SLOTS
+
+    def enqueue_ionic(self, order, mask, head):
+        """The ionic section of the step (simulation.py:440-455): one launch
+        per volume, plus the combo/x0 prep pass when it is not fused."""
         lib = N.lib()
         stream = self._stream
-        head = self.head
-        nslot = (head + 1) % RING_SLOTS
-        timed = self.timed
-        if timed:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            ev[0].record()
         if not self.fused_prep:
             ia = self._prep_args
             ia.head, ia.order, ia.active_mask = head, order, mask
@@ -580,11 +571,10 @@ class TissueSolver:
             N.check(lib.mdx_tissue_ionic(model_id, N.C.byref(ia), Pp, int(Ph.size), stream),
                     "mdx_tissue_ionic")
             self.launches += 1
-        if timed:
-            ev[1].record()
-        if events is not None:
-            events[0].record()
 
+    def solve_args(self, order, t_next, head, nslot):
+        """The solve's argument block for this step (system of this BDF
+        order, x = the next ring slot, iteration/residual log slots)."""
         a = self._cg_args
         a.a_val = self._a_ptr[order]
         a.dinv = self._dinv_ptr[order]
@@ -599,6 +589,33 @@ class TissueSolver:
             self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
         a.iters_out = self._log_ptrs[0] + 4 * slot
         a.relres_out = self._log_ptrs[1] + 8 * slot
+        return a
+
+    def enqueue_step(self, events=None, record=None):
+        """Launch one step; no host synchronisation.
+
+        `events`: optional (after_ionic, after_solve) CUDA events recorded on
+        the launch stream (bench.py's per-kernel timing).
+        `record`: optional (probe_idx, dst): the solve itself writes the run()
+        output row [u_min, u_max, u[probes]] of the new potential into `dst`
+        (a pinned host float64 row, written through its device mapping, or a
+        CUDA tensor) - no extra kernel or copy.
+        """
+        import torch
+
+        order, t_next, mask, head, nslot = self.step_plan()
+        lib = N.lib()
+        stream = self._stream
+        timed = self.timed
+        if timed:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+        self.enqueue_ionic(order, mask, head)
+        if timed:
+            ev[1].record()
+        if events is not None:
+            events[0].record()
+        a = self.solve_args(order, t_next, head, nslot)
         if record is not None:
             probe_idx, dst = record
             k = 2 + (0 if probe_idx is None else probe_idx.numel())
@@ -622,6 +639,10 @@ class TissueSolver:
             self.timer.device_span("Ionic model update", ev[0], ev[1])
             self.timer.device_span("Linear solver", ev[1], ev[2])
 
+        self.advance_bookkeeping(head, nslot, t_next)
+
+    def advance_bookkeeping(self, head, nslot, t_next):
+        """Ring pushes and time accumulation (simulation.py:477-482)."""
         self._pending.append((self.step_index, head, self.time))
         self.head = nslot
         self.u_fill = min(self.u_fill + 1, 3)

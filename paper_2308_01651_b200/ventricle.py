@@ -68,7 +68,8 @@ def prolate_ventricle(n_xi, n_th, n_ph, apex_opening=1e-3):
     xi_idx = (tets % nx1).sum(axis=1)                       # 4 * centroid_xi * n_xi
     cxi = xi_idx / (4.0 * n_xi)
     mats = np.where(cxi < 1.0 / 3.0, 1, np.where(cxi < 2.0 / 3.0, 2, 3)).astype(np.int32)
-    mesh = Mesh(nodes, tets, ElementKind.TET4, mats)
+    mesh = Mesh(nodes, tets, ElementKind.TET4, mats,
+                grid=((nx1, nt1, n_ph), (False, False, True)))
 
     # fiber frame from the analytic tangents
     a = INNER_A + WALL * XI

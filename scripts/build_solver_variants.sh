@@ -10,7 +10,7 @@ while [ $# -gt 0 ]; do
   name=$1; flags=$2; shift 2
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     -I include --expt-relaxed-constexpr $flags -c paper_2308_01651_b200/csrc/solver.cu \
-    -o $B/variants/solver_$name.o -Xptxas -v 2>&1 | grep -A2 "pcg_kernelILi1ELb1ELi[0-9]ELb1" | grep -E "registers|spill" | head -2 | sed "s/^/[$name] /"
+    -o $B/variants/solver_$name.o -Xptxas -v 2>&1 | grep -A2 "pcg_kernelILi263ELb1ELi4ELb0" | grep -E "registers|spill" | head -2 | sed "s/^/[$name] /"
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $B/ionic.o \
     $B/assembly.o $B/variants/solver_$name.o -o $B/variants/libmdx_$name.so
   rm -f $B/variants/solver_$name.o

@@ -1,10 +1,10 @@
 """Multi-rank host logic of the distributed solver, on CPU over gloo.
 
-The partition/halo/pipelined-PCG/step logic of
-paper_2308_01651_b200.distributed runs in 2 (and 3) processes with the CPU
-hook implementation of tests/dist_cpu.py; the gathered potential, CG
-iteration counts and activation map must match the single-domain oracle
-(which is pinned bit-for-bit to the reference).
+The RCB partition, rank-local problems, halo plans/exchange and the
+pipelined-PCG drivers of paper_2308_01651_b200.distributed run in 2 and 3
+processes with the CPU hooks of tests/dist_cpu.py; the gathered potential,
+CG iteration counts and activation map must match the single-domain oracle
+(pinned bit-for-bit to the reference) on configs 0, 3 and 4 (reduced sizes).
 """
 
 import os
@@ -14,49 +14,85 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2308_01651_b200.distributed import slab_partition
+from paper_2308_01651_b200.partition import (build_part, grid_coords, grid_of, halo_plans,
+                                             partition, rcb, send_lists)
 
 
-def test_slab_partition_covers_lattice_once():
-    for lattice, nr in (((40, 14, 6), 2), ((40, 14, 6), 3), ((200, 70, 30), 8),
-                        ((4, 4, 4), 5)):
-        slabs = slab_partition(lattice, nr)
-        plane = (lattice[0] + 1) * (lattice[1] + 1)
-        owned = np.concatenate([s.owned_global for s in slabs])
-        assert np.array_equal(owned, np.arange(plane * (lattice[2] + 1)))
-        for s in slabs:
-            assert s.k1 > s.k0
-            assert s.n_local == (s.kl1 - s.kl0) * plane
-            # every halo send range is owned, every recv range is a ghost plane
-            for peer, (a0, a1), (b0, b1) in s.halo_plan():
-                assert s.own_begin <= a0 < a1 <= s.own_end
-                assert b1 <= s.own_begin or b0 >= s.own_end
-                assert a1 - a0 == b1 - b0 == plane
-                other = slabs[peer]
-                assert any(p == s.rank for p, _, _ in other.halo_plan())
+def _cfg(name):
+    from paper_2308_01651_b200 import configs, ventricle
+
+    ns = configs.this_package()
+    if name == "cfg0":
+        return configs.config0(ns, h=1e-3)
+    if name == "cfg3":
+        return configs.config3(ns, h=1e-3, seed=7)
+    if name == "cfg4":
+        return ventricle.config4(ns, n_xi=3, n_th=12, n_ph=32)
+    raise KeyError(name)
+
+
+def test_rcb_balanced_deterministic():
+    rng = np.random.default_rng(0)
+    pts = rng.standard_normal((1000, 3)) * (5.0, 1.0, 0.2)
+    for k in (1, 2, 3, 5, 8):
+        p = rcb(pts, k)
+        sizes = np.bincount(p, minlength=k)
+        assert sizes.sum() == 1000 and sizes.min() >= 1000 // k - 1
+        assert sizes.max() <= -(-1000 // k) + 1
+        np.testing.assert_array_equal(p, rcb(pts, k))
+    # the first cut is across the longest axis
+    p = rcb(pts, 2)
+    assert pts[p == 0, 0].max() <= pts[p == 1, 0].min()
     with pytest.raises(ValueError):
-        slab_partition((4, 4, 2), 4)
+        rcb(pts[:3], 4)
 
 
-def test_sweep_split_rows():
-    """Interior rows never read a ghost plane; interior + boundary = owned."""
-    for lattice, nr in (((40, 14, 6), 2), ((40, 14, 6), 3), ((200, 70, 30), 8),
-                        ((4, 4, 3), 4), ((4, 4, 4), 1)):
-        plane = (lattice[0] + 1) * (lattice[1] + 1)
-        for s in slab_partition(lattice, nr):
-            sp = s.sweep_split()
-            ghosts = [(r0, r1) for _, _, (r0, r1) in s.halo_plan()]
-            if sp is None:
-                assert not ghosts or s.k1 - s.k0 <= len(ghosts)
-                continue
-            (i0, i1), bnd = sp
-            rows = sorted([(i0, i1)] + bnd)
-            assert rows[0][0] == s.own_begin and rows[-1][1] == s.own_end
-            assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
-            # the interior's stencil reach (one plane either side) misses the ghosts
-            for g0, g1 in ghosts:
-                assert i1 + plane <= g0 or i0 - plane >= g1
-            assert len(bnd) == len(ghosts)
+@pytest.mark.parametrize("name", ["cfg0", "cfg3", "cfg4"])
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_local_problems(name, nranks):
+    """Every owned node's element star is local; send/recv lists agree
+    between ranks; on logical grids every part is a box whose local operator
+    pattern compresses to the same diagonals as the global one."""
+    import torch
+
+    from paper_2308_01651_b200.fem import FeSpace
+    from paper_2308_01651_b200.operators import DiaOperator
+
+    mesh = _cfg(name).mesh
+    owner = partition(mesh, nranks)
+    assert np.bincount(owner).min() > 0
+    g = grid_of(mesh)
+    assert g is not None
+    parts = halo_plans(mesh, owner)
+    el = mesh.elements
+    n_glob_pat = FeSpace(mesh).pattern()
+    glob_plan = DiaOperator.plan(torch.from_numpy(n_glob_pat[0]),
+                                 torch.from_numpy(n_glob_pat[1]), mesh.num_nodes)
+    for p in parts:
+        own = np.flatnonzero(owner == p.rank)
+        np.testing.assert_array_equal(np.sort(p.nodes[p.owned]), own)
+        star = np.flatnonzero(np.isin(el, own).any(axis=1))
+        assert np.isin(star, p.elements).all()
+        assert np.all(np.diff(p.elements) > 0)              # ascending global order
+        np.testing.assert_array_equal(mesh.elements[p.elements], p.nodes[p.conn])
+        # a part is a logical box: its owned coordinates span a product range
+        c = grid_coords(g[0], own)
+        span = np.prod([np.unique(c[:, a]).size for a in range(3)])
+        assert span == own.size
+        # the product's communication-free send lists equal the plan's
+        sl = send_lists(mesh, owner, p)
+        assert sorted(sl) == sorted(p.send)
+        for q in sl:
+            np.testing.assert_array_equal(sl[q], p.send[q])
+            other = parts[q]
+            np.testing.assert_array_equal(p.nodes[p.send[q]], other.nodes[other.recv[p.rank]])
+        # local pattern: diagonal structure kept
+        from paper_2308_01651_b200.geometry import Mesh
+
+        loc = Mesh(mesh.nodes[p.nodes], p.conn, mesh.element_kind, mesh.material_ids[p.elements])
+        ip, ix = FeSpace(loc).pattern()
+        plan = DiaOperator.plan(torch.from_numpy(ip), torch.from_numpy(ix), loc.num_nodes)
+        assert plan is not None and len(plan["pos"]) <= len(glob_plan["pos"])
 
 
 def _free_port():
@@ -65,7 +101,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, steps, out_dir, device_scalars=False):
+def _worker(rank, world, port, name, steps, out_dir, device_scalars):
     import sys
     from pathlib import Path
 
@@ -73,42 +109,37 @@ def _worker(rank, world, port, steps, out_dir, device_scalars=False):
     sys.path.insert(0, str(Path(__file__).resolve().parent))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["MDX_DIST_OVERLAP_MIN"] = "0"     # exercise the split on the small slab
+    os.environ["OMP_NUM_THREADS"] = "1"
     import torch.distributed as dist
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from dist_cpu import CpuSlabTissue
-        from paper_2308_01651_b200 import configs
+        from dist_cpu import CpuPartTissue
 
-        cfg = configs.config0(configs.this_package(), h=1e-3)
-        solver = CpuSlabTissue(cfg, device_scalars=device_scalars)
+        solver = CpuPartTissue(_cfg(name), device_scalars=device_scalars)
         for _ in range(steps):
             solver.step()
         u = solver.gather_potential()
-        sl = solver.slab
-        act = solver.act.copy()
-        frozen = solver.frozen.copy()
-        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u,
-                 iters=np.array(solver.iters),
-                 act=act[sl.own_begin:sl.own_end],
-                 frozen=frozen[sl.own_begin:sl.own_end],
-                 split_rows=np.array(sorted(solver.sweep_rows_seen)).reshape(-1, 2))
+        amap = solver.gather_activation_map()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u, act=amap,
+                 iters=np.array(solver.iters), sel=np.array(sorted(solver.sel_seen)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,device_scalars", [(2, False), (3, False), (2, True), (3, True)])
-def test_distributed_step_matches_single_domain_oracle(tmp_path, world, device_scalars):
-    """Host-driven (PipelinedPcgDriver) and device-scalar (DevicePcgDriver:
-    chunked enqueue, phases gated on the scalar state) distributed steps."""
+@pytest.mark.parametrize("name,world,device_scalars,steps", [
+    ("cfg0", 2, False, 60), ("cfg0", 3, True, 60),
+    ("cfg3", 2, True, 40), ("cfg3", 3, False, 40),
+    ("cfg4", 2, True, 40), ("cfg4", 3, True, 40)])
+def test_distributed_step_matches_single_domain_oracle(tmp_path, name, world, device_scalars,
+                                                       steps):
+    """Host-driven (PipelinedPcgDriver) and device-scalar (DevicePcgDriver)
+    distributed steps against the single-domain oracle."""
     from oracle import monodomain_oracle as O
-    from paper_2308_01651_b200 import configs
 
-    steps = 60
-    mp.spawn(_worker, args=(world, _free_port(), steps, str(tmp_path), device_scalars),
+    mp.spawn(_worker, args=(world, _free_port(), name, steps, str(tmp_path), device_scalars),
              nprocs=world, join=True)
-    cfg = configs.config0(configs.this_package(), h=1e-3)
+    cfg = _cfg(name)
     orc = O.OracleTissue(cfg)
     for _ in range(steps):
         orc.step()
@@ -116,20 +147,15 @@ def test_distributed_step_matches_single_domain_oracle(tmp_path, world, device_s
     for r in res:
         np.testing.assert_array_equal(r["u"], res[0]["u"])           # all ranks agree
         np.testing.assert_array_equal(r["iters"], res[0]["iters"])
-    if world == 2:
-        # every rank swept its interior plane during the halo exchange and its
-        # plane next to the ghost after it (distributed.py sweep overlap)
-        for r in res:
-            assert len(r["split_rows"]) == 2, r["split_rows"]
+        # interior rows swept during the halo exchange, boundary rows after it
+        assert set(r["sel"].tolist()) == {1, 2}, r["sel"]
     its = res[0]["iters"]
     assert np.abs(its - np.array(orc.iters)).max() <= 1
     u = res[0]["u"]
     rel = np.linalg.norm(u - orc.potential) / np.linalg.norm(orc.potential)
     assert rel < 1e-9, rel
-    act = np.concatenate([r["act"] for r in res])
-    frozen = np.concatenate([r["frozen"] for r in res]).astype(bool)
-    amap = np.where(frozen, act, -1.0)
-    ref = orc.activation_map
+    amap, ref = res[0]["act"], orc.activation_map
     assert np.array_equal(amap >= 0, ref >= 0)
     both = (amap >= 0) & (ref >= 0)
-    assert np.abs(amap[both] - ref[both]).max() <= cfg.dt * (1 + 1e-9)
+    if both.any():
+        assert np.abs(amap[both] - ref[both]).max() <= cfg.dt * (1 + 1e-9)

@@ -513,15 +513,25 @@ def test_ttp06_slab_cg_variants(golden, ns, variant):
     assert _rel(s.potential, g["final_u"]) < 1e-8
 
 
-def test_distributed_solver_single_rank_on_gpu(golden, ns):
-    """DistributedTissueSolver (phase kernels + NCCL plumbing) with one rank
-    reproduces the reference config-0 run (multi-rank host logic: gloo tests)."""
+def _dist_cfg(name):
+    from paper_2308_01651_b200 import configs, ventricle
+
+    ns = configs.this_package()
+    if name == "tissue_cfg0":
+        return configs.config0(ns)
+    return ventricle.config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3)
+
+
+@pytest.mark.parametrize("name,steps", [("tissue_cfg0", 300), ("tissue_cfg4_small", 500)])
+def test_distributed_solver_single_rank_on_gpu(golden, name, steps):
+    """DistributedTissueSolver (rank-local TissueSolver, phase kernels with
+    row classes, NCCL plumbing) with one rank reproduces the reference run
+    (multi-rank host logic: tests/test_distributed.py over gloo)."""
     import os
     import socket
 
     import torch.distributed as dist
 
-    from paper_2308_01651_b200 import configs
     from paper_2308_01651_b200.distributed import DistributedTissueSolver
 
     with socket.socket() as s:
@@ -531,19 +541,18 @@ def test_distributed_solver_single_rank_on_gpu(golden, ns):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
-        g = golden("tissue_cfg0")
-        s = DistributedTissueSolver(configs.config0(ns))
-        for _ in range(300):
+        g = golden(name)
+        s = DistributedTissueSolver(_dist_cfg(name))
+        for _ in range(steps):
             s.step()
         its = np.array(s.iters)
-        assert np.abs(its - g["iters"][:300]).max() <= 1
-        u = s.gather_potential()
-        assert _rel(u, g["snap_300"]) < 1e-9
+        assert np.abs(its - g["iters"][:steps]).max() <= 1
+        assert _rel(s.gather_potential(), g[f"snap_{steps}"]) < 1e-9
     finally:
         dist.destroy_process_group()
 
 
-def _gloo_gpu_worker(rank, world, port, steps, out_dir):
+def _gloo_gpu_worker(rank, world, port, name, steps, out_dir):
     import os
     import sys
     from pathlib import Path
@@ -551,28 +560,31 @@ def _gloo_gpu_worker(rank, world, port, steps, out_dir):
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["MDX_DIST_OVERLAP_MIN"] = "0"     # exercise the halo/interior split
     import torch.distributed as dist
 
-    from paper_2308_01651_b200 import configs
     from paper_2308_01651_b200.distributed import DistributedTissueSolver
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        s = DistributedTissueSolver(configs.config0(configs.this_package()))
+        s = DistributedTissueSolver(_dist_cfg(name))
         for _ in range(steps):
             s.step()
         u = s.gather_potential()
-        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u, iters=np.array(s.iters))
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), u=u, iters=np.array(s.iters),
+                 act=s.gather_activation_map(), kind=np.array(s.local.op.kind))
     finally:
         dist.destroy_process_group()
 
 
-def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path):
-    """The multi-rank GPU path (slab partition, ghost planes, device-scalar
-    pipelined PCG, phase kernels on a local slab) with two ranks sharing the
-    one GPU of the box.  Exchanges go through gloo host staging, so no rank's
-    kernels wait on another's; NCCL itself is covered by the single-rank test."""
+@pytest.mark.parametrize("name,steps,kind", [("tissue_cfg0", 200, 1),
+                                             ("tissue_cfg4_small", 500, 4)])
+def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path, name, steps, kind):
+    """The multi-rank GPU path (RCB boxes, rank-local problems: class-table
+    stencil on the slab, diagonal operator on the ventricle; device-scalar
+    pipelined PCG with the interior sweep overlapping the halo) with two
+    ranks sharing the one GPU of the box.  Exchanges go through gloo host
+    staging, so no rank's kernels wait on another's; NCCL itself is covered
+    by the single-rank test."""
     import socket
 
     import torch.multiprocessing as mp
@@ -580,14 +592,15 @@ def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    steps = 200
-    mp.spawn(_gloo_gpu_worker, args=(2, port, steps, str(tmp_path)), nprocs=2, join=True)
-    g = golden("tissue_cfg0")
+    mp.spawn(_gloo_gpu_worker, args=(2, port, name, steps, str(tmp_path)), nprocs=2,
+             join=True)
+    g = golden(name)
     res = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
     np.testing.assert_array_equal(res[0]["u"], res[1]["u"])
     np.testing.assert_array_equal(res[0]["iters"], res[1]["iters"])
+    assert int(res[0]["kind"]) == kind
     assert np.abs(res[0]["iters"] - g["iters"][:steps]).max() <= 1
-    assert _rel(res[0]["u"], g["snap_200"]) < 1e-9
+    assert _rel(res[0]["u"], g[f"snap_{steps}"]) < 1e-9
 
 
 def test_fused_output_row(ns):
