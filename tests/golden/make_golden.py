@@ -256,6 +256,76 @@ def tissue(name, build, steps, snap_every=None, payload_at=(), subsample=None, l
     print(f"{name}: {steps} steps in {wall:.1f} s, iters {its.min()}..{its.max()}")
 
 
+def tissue_segmented(name, build, steps, seg=500, subsample=97, work="/tmp/golden_seg"):
+    """Long full-size runs (config 3: 25,000 steps, hours of CPU): the unmodified
+    reference stepped in segments of `seg` steps; after each segment the records so
+    far and the reference's own checkpoint payload go to `work`, so an interrupted
+    run resumes through `TissueSolver.restore` (bit-exact: the payload carries every
+    history ring and the activation fields, reference simulation.py:518-607).
+    Records: per-step CG iterations / probe potentials / u_min / u_max, snapshots
+    every `seg` steps (every `subsample`-th node), activation map as step numbers."""
+    configs, ns = _ref()
+    from monodomain.simulation import TissueSolver
+
+    cfg = build(configs, ns)
+    pts = configs.corner_probes() + [(10e-3, 3.5e-3, 1.5e-3)]
+    probes = [ns.nearest_node(cfg.mesh, p) for p in pts]
+    solver = TissueSolver(cfg)
+    wdir = Path(work) / name
+    wdir.mkdir(parents=True, exist_ok=True)
+    its = np.zeros(steps, dtype=np.int16)
+    pr = np.zeros((steps, len(probes)))
+    umin = np.zeros(steps)
+    umax = np.zeros(steps)
+    snaps = {}
+    done = 0
+    state = wdir / "state.npz"
+    if state.exists():
+        z = np.load(state)
+        done = int(z["done"])
+        its[:done], pr[:done] = z["iters"][:done], z["probe_u"][:done]
+        umin[:done], umax[:done] = z["umin"][:done], z["umax"][:done]
+        snaps = {int(k[5:]): z[k] for k in z.files if k.startswith("snap_")}
+        solver.restore((wdir / "payload.bin").read_bytes())
+        assert solver.step_index == done
+        print(f"{name}: resumed at step {done}", flush=True)
+    t0 = time.perf_counter()
+    while done < steps:
+        for k in range(done, min(done + seg, steps)):
+            u = solver.step()
+            its[k] = solver.last_iterations
+            pr[k] = u[probes]
+            umin[k], umax[k] = u.min(), u.max()
+        done = k + 1
+        snaps[done] = u[::subsample].copy()
+        (wdir / "payload.tmp").write_bytes(solver.checkpoint_payload())
+        np.savez(wdir / "state.tmp.npz", done=np.array(done), iters=its, probe_u=pr,
+                 umin=umin, umax=umax, **{f"snap_{s}": v for s, v in snaps.items()})
+        (wdir / "payload.tmp").rename(wdir / "payload.bin")
+        (wdir / "state.tmp.npz").rename(state)
+        _write_segmented(name, cfg, solver, done, its, pr, umin, umax, snaps, probes,
+                         subsample)
+        print(f"{name}: step {done}/{steps}, {time.perf_counter() - t0:.0f} s, "
+              f"iters {its[done - seg:done].min()}..{its[done - seg:done].max()}, "
+              f"frozen {int(solver.frozen.sum())}", flush=True)
+
+
+def _write_segmented(name, cfg, solver, done, its, pr, umin, umax, snaps, probes, subsample):
+    act = solver.activation_map
+    u = solver.potential
+    out = dict(iters=its[:done], probes=np.asarray(probes), probe_u=pr[:done],
+               umin=umin[:done], umax=umax[:done], steps=np.array(done),
+               activation=np.where(act < 0, -1, np.rint(act / cfg.dt)).astype(np.int32),
+               act_steps=np.array(1), frozen=solver.frozen.astype(np.uint8),
+               final_u_sha=np.array(sha(u)), final_u_sub=u[::subsample],
+               subsample=np.array(subsample))
+    for s, v in snaps.items():
+        out[f"snap_{s}"] = v
+    tmp = OUT / f"{name}.tmp.npz"
+    np.savez_compressed(tmp, **out)
+    tmp.rename(OUT / f"{name}.npz")
+
+
 def cfg1_subset():
     """Config 1 parity subset: seeded TTP06 cells, 0D splitting, BDF1/BDF2."""
     from monodomain.ionic import IonicModelSpec, ModelKind, model_module
@@ -343,9 +413,10 @@ JOBS = {
                                  fromlist=["size_for_nodes"]).size_for_nodes(100_000),
                  final_time=60e-3), 3000, snap_every=250, subsample=7, lean=True,
         act_steps=True),
-    "tissue_cfg3_full": lambda: tissue("tissue_cfg3_full", lambda c, ns: c.config3(ns),
-                                       25000, snap_every=500, subsample=97, lean=True,
-                                       act_steps=True),
+    # resumable: `python make_golden.py tissue_cfg3_full` again continues from the
+    # last finished segment; the fixture on disk always holds the steps done so far
+    "tissue_cfg3_full": lambda: tissue_segmented("tissue_cfg3_full",
+                                                 lambda c, ns: c.config3(ns), 25000),
 }
 
 if __name__ == "__main__":

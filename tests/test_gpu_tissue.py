@@ -392,6 +392,24 @@ def test_cfg2_full_run_5000_steps(golden, ns):
     assert (g["activation"] >= 0).all()            # the whole slab activates
 
 
+def test_cfg3_full_size_25000_steps(golden, ns):
+    """Config 3 at its stated size AND length (442,401 nodes, three volumes with
+    duplicated interface states, scar sigma x0.01, second stimulus at 0.3 s,
+    25,000 steps = 500 ms) against the unmodified reference: per-step CG
+    iterations, per-step probe traces, 50 snapshots, the full activation map."""
+    from paper_2308_01651_b200 import configs
+
+    g = golden("tissue_cfg3_full")
+    steps = int(g["steps"])
+    assert steps == 25000
+    s, pu, snaps = _run_long(g, configs.config3(ns), steps)
+    assert len(s.volumes) == 3
+    its = _check_long(s, pu, snaps, g, steps, 2e-5)
+    assert (its == g["iters"]).mean() > 0.95
+    # the second pulse (t = 0.3 s, step 15,000) re-excites the slab
+    assert g["iters"][15000:15200].max() > 10 and its[15000:15200].max() > 10
+
+
 def test_cfg4_ventricle_100k_60ms(golden, ns):
     """Config 4 geometry reduced to 128,700 nodes (P1 tets, 3 volumes with
     duplicated interface states, helix fibers) over 60 ms (3,000 steps), on
