@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define MDX_ABI_VERSION 4
+#define MDX_ABI_VERSION 5
 
 #define MDX_OK 0
 #define MDX_ERR_ARG (-1)
@@ -34,6 +34,21 @@ extern "C" {
 #define MDX_MODEL_ALIEV_PANFILOV 0
 #define MDX_MODEL_BUENO_OROVIO 1
 #define MDX_MODEL_TTP06 2
+
+/* Ionic time integrator.  MDX_GATES_BDF is the reference's scheme (closed-form
+ * implicit BDF gate solve, explicit BDF non-gates: <model>.advance_kernel).
+ * MDX_GATES_RUSH_LARSEN is the mode BASELINE.json's north_star / config 1 name
+ * and the reference does not have: from W_n alone,
+ * gates w+ = w_inf + (w_n - w_inf) exp(-dt/tau), non-gates explicit Euler, with
+ * the reference's own targets/currents/rates (ten_tusscher.py:175-350,
+ * bueno_orovio.py:101-132) and the same [0,1] clamp. */
+#define MDX_GATES_BDF 0
+#define MDX_GATES_RUSH_LARSEN 1
+
+/* bits of the status word the step kernels raise (mdx_cg_args.status) */
+#define MDX_STATUS_DIVERGED 1
+#define MDX_STATUS_NONFINITE 2
+#define MDX_STATUS_STOPPED 4
 
 #define MDX_OP_STENCIL27 1 /* structured hex slab, node-class tables */
 #define MDX_OP_CSR 2       /* assembled CSR, int64 indptr / int32 indices */
@@ -71,6 +86,12 @@ int mdx_ionic_advance(int model, int64_t n, const double* u_ext, const double* W
                       const double* W_bdf, int64_t cs, int64_t vs, double alpha, double dt,
                       const double* P, int np, double* W_out, double* I_out,
                       unsigned long long* clamp_count, void* stream);
+
+/* Rush-Larsen counterpart of advance_kernel (MDX_GATES_RUSH_LARSEN above): W_out from
+ * W_n at potential u, I_out = I_ion(u, W_out).  Same layout/ownership rules. */
+int mdx_ionic_advance_rl(int model, int64_t n, const double* u, const double* W_n, int64_t cs,
+                         int64_t vs, double dt, const double* P, int np, double* W_out,
+                         double* I_out, unsigned long long* clamp_count, void* stream);
 
 /* <model>.current_kernel(u, W, P, I_out)
  *   bueno_orovio.py:146-149, ten_tusscher.py:368-371, aliev_panfilov.py:75-79 */
@@ -111,7 +132,7 @@ typedef struct mdx_tissue_ionic_args {
   int64_t ldp;
   uint64_t active_mask;  /* impulses whose window is open at t_{n+1} */
   int32_t n_impulses;
-  int32_t _pad;
+  int32_t gate_scheme;   /* MDX_GATES_BDF (reference) or MDX_GATES_RUSH_LARSEN */
   const int32_t* status; /* nonzero => an earlier step failed: no-op */
 } mdx_tissue_ionic_args;
 
@@ -189,7 +210,8 @@ typedef struct mdx_cg_args {
   unsigned long long* barrier; /* grid-barrier counter, zero-initialised, reused */
   int32_t* iters_out;    /* iterations (reference convention: -max_iter) */
   double* relres_out;
-  int32_t* status;       /* nonzero on entry => no-op; bit0 diverged, bit1 non-finite */
+  int32_t* status;       /* nonzero on entry => no-op; bit0 diverged, bit1 non-finite,
+                            bit2 (MDX_STATUS_STOPPED) fully activated, see below */
   int32_t* fail_step;    /* receives `step` when status is raised */
   int32_t variant;       /* 0: reference recurrences (3 syncs/iter); 1: q = A z + beta q (2);
                             2: pipelined PCG (1 reduction/iter) */
@@ -220,6 +242,22 @@ typedef struct mdx_cg_args {
   const uint8_t* row_mask;
   int32_t row_select;
   int32_t _pad3;
+  /* ABI v5, optional (NULL = off): 4 globaltimer stamps [ns] written by block 0 of
+     mdx_pcg_solve: kernel start, RHS + initial residual done ("Monodomain
+     assembly", simulation.py:457-465), CG loop done ("Linear solver"), activation
+     and output row done ("Other") - the reference's per-step sections
+     (simulation.py:225-254, 432-483) from inside the fused kernel */
+  unsigned long long* tstamps;
+  /* ABI v5, optional (NULL = off): *frozen_count accumulates the nodes whose
+     activation time froze (simulation.py:485-494).  With stop_when_full != 0 the
+     step that brings it to frozen_target stores its index in *fail_step and sets
+     bit 2 (MDX_STATUS_STOPPED) of *status: later launches on the stream are
+     no-ops, which is run(stop_when_fully_activated=True) (simulation.py:702-703)
+     without a host synchronisation per step */
+  unsigned long long* frozen_count;
+  int64_t frozen_target;
+  int32_t stop_when_full;
+  int32_t _pad4;
 } mdx_cg_args;
 
 /* blocks_hint: grid size override (0 = automatic, capped at one co-resident wave) */
@@ -328,6 +366,8 @@ typedef struct mdx_pace_args {
   double* trace;         /* [n_trace_cells][trace_rows][2+nv] */
   unsigned long long* clamp_count;
   int32_t* status;       /* bit0: a cell lost finiteness */
+  int32_t gate_scheme;   /* MDX_GATES_BDF, or MDX_GATES_RUSH_LARSEN (order must be 1) */
+  int32_t _pad;
 } mdx_pace_args;
 
 int mdx_pace_cells(int model, const mdx_pace_args* args, const double* P, int np,

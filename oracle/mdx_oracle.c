@@ -227,6 +227,51 @@ static void ttp_advance1(double u, const double* we, const double* wb, double al
   *I = ttp_total(&co);
 }
 
+/* ------------------------------------------------------------------ */
+/* Rush-Larsen mode (BASELINE.json north_star / config 1).  The reference has */
+/* no such integrator: this restates ONLY the integrator, over  */
+/* the reference functions restated above (_gate_targets / _gate_pieces,      */
+/* _currents, _conc_rates, _total).  Pinned by tests/golden/rl_kat.npz, which */
+/* tests/golden/make_golden.py builds by calling the reference's own jitted   */
+/* functions with the same integrator.                                        */
+/*   gates      w+ = inf + (w_n - inf) * exp(-dt_ms / tau), clamped to [0,1]  */
+/*   non-gates  w+ = w_n + dt_ms * rate(v, W_n)                               */
+/*   I          = total(currents(v, W+))                                      */
+/* ------------------------------------------------------------------ */
+static void ttp_rl1(double u, const double* wn, double dt, const double* P, double* wo,
+                    double* I, int* nc) {
+  double dtm = dt * 1.0e3, v = u * 1.0e3, inf[12], tau[12], cr[6];
+  ttp_targets(v, wn[14], P[49], inf, tau);
+  for (int g = 0; g < 12; ++g) {
+    double x = inf[g] + (wn[g] - inf[g]) * exp(-dtm / tau[g]);
+    if (x < 0.0) { x = 0.0; ++*nc; } else if (x > 1.0) { x = 1.0; ++*nc; }
+    wo[g] = x;
+  }
+  ttp_cur ce = ttp_currents(v, wn, P);
+  ttp_conc(wn, &ce, P, cr);
+  for (int k = 0; k < 6; ++k) wo[12 + k] = wn[12 + k] + dtm * cr[k];
+  ttp_cur co = ttp_currents(v, wo, P);
+  *I = ttp_total(&co);
+}
+
+static void bo_rl1(double u, const double* wn, double dt, const double* P, double* wo,
+                   double* I, int* nc) {
+  double dtm = dt * 1.0e3, src[3], rate[3];
+  bo_pieces(u, P, src, rate);
+  for (int g = 0; g < 3; ++g) {
+    double inf = src[g] / rate[g];
+    double x = inf + (wn[g] - inf) * exp(-dtm * rate[g]);
+    if (x < 0.0) { x = 0.0; ++*nc; } else if (x > 1.0) { x = 1.0; ++*nc; }
+    wo[g] = x;
+  }
+  *I = bo_current(u, wo[0], wo[1], wo[2], P);
+}
+
+static void apf_rl1(double u, const double* wn, double dt, const double* P, double* wo,
+                    double* I, int* nc) {
+  apf_advance1(u, wn, wn, 1.0, dt, P, wo, I, nc); /* no gates: explicit Euler */
+}
+
 typedef void (*advance_fn)(double, const double*, const double*, double, double,
                            const double*, double*, double*, int*);
 
@@ -245,6 +290,22 @@ long orc_advance(int model, long n, const double* u, const double* We, const dou
   for (long i = 0; i < n; ++i) {
     int nc = 0;
     f(u[i], We + i * nv, Wb + i * nv, alpha, dt, P, Wo + i * nv, Io + i, &nc);
+    total += nc;
+  }
+  return total;
+}
+
+/* Rush-Larsen step over n cells, AoS (n, nv) arrays; returns the clamp count */
+long orc_advance_rl(int model, long n, const double* u, const double* Wn, double dt,
+                    const double* P, double* Wo, double* Io) {
+  const int nv = model_nv(model);
+  long total = 0;
+#pragma omp parallel for reduction(+ : total) schedule(static)
+  for (long i = 0; i < n; ++i) {
+    int nc = 0;
+    if (model == 0) apf_rl1(u[i], Wn + i * nv, dt, P, Wo + i * nv, Io + i, &nc);
+    else if (model == 1) bo_rl1(u[i], Wn + i * nv, dt, P, Wo + i * nv, Io + i, &nc);
+    else ttp_rl1(u[i], Wn + i * nv, dt, P, Wo + i * nv, Io + i, &nc);
     total += nc;
   }
   return total;

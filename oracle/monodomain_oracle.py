@@ -53,6 +53,8 @@ def lib():
         _lib.orc_advance.argtypes = [C.c_int, C.c_long, P, P, P, C.c_double, C.c_double,
                                      P, P, P]
         _lib.orc_advance.restype = C.c_long
+        _lib.orc_advance_rl.argtypes = [C.c_int, C.c_long, P, P, C.c_double, P, P, P]
+        _lib.orc_advance_rl.restype = C.c_long
         _lib.orc_current.argtypes = [C.c_int, C.c_long, P, P, P, P]
         _lib.orc_csr_matvec.argtypes = [C.c_long, P, P, P, P, P]
         _lib.orc_cg.argtypes = [C.c_long, P, P, P, P, P, P, C.c_double, C.c_long, P, P]
@@ -90,6 +92,16 @@ def advance(model_name, u_ext, W_ext, W_bdf, alpha, dt, P, W_out, I_out):
     return int(lib().orc_advance(_MODEL_ID[model_name], u_ext.shape[0], _p(u_ext),
                                  _p(W_ext), _p(W_bdf), alpha, dt, _p(P), _p(W_out),
                                  _p(I_out)))
+
+
+def advance_rl(model_name, u, W_n, dt, P, W_out, I_out):
+    """Rush-Larsen one-step update (mdx_oracle.c: ttp_rl1 / bo_rl1 / apf_rl1):
+    only the integrator differs from `advance`; pinned by tests/golden/rl_kat.npz."""
+    u = np.ascontiguousarray(u, np.float64)
+    W_n = np.ascontiguousarray(W_n, np.float64)
+    P = np.ascontiguousarray(P, np.float64)
+    return int(lib().orc_advance_rl(_MODEL_ID[model_name], u.shape[0], _p(u), _p(W_n), dt,
+                                    _p(P), _p(W_out), _p(I_out)))
 
 
 def current(model_name, u, W, P, I_out):
@@ -246,9 +258,11 @@ class _Vol:
 class OracleTissue:
     """Reference time loop on the CPU (numpy + mdx_oracle.c)."""
 
-    def __init__(self, config):
+    def __init__(self, config, gate_scheme="bdf"):
         cfg = config
         self.cfg = cfg
+        assert gate_scheme in ("bdf", "rush_larsen")
+        self.gate_scheme = gate_scheme
         mesh = cfg.mesh
         n = mesh.nodes.shape[0]
         self.n = n
@@ -378,8 +392,12 @@ class OracleTissue:
             we = self._wsum(v.ring, ew)
             wo = np.empty_like(we)
             io = np.empty(v.dofs.size)
-            self.clamps += advance(v.model, u_ext[v.dofs], we, wb, alpha, self.dt, v.P,
-                                   wo, io)
+            if self.gate_scheme == "rush_larsen":     # one step from W_n at u_EXT
+                self.clamps += advance_rl(v.model, u_ext[v.dofs], v.ring[0], self.dt, v.P,
+                                          wo, io)
+            else:
+                self.clamps += advance(v.model, u_ext[v.dofs], we, wb, alpha, self.dt, v.P,
+                                       wo, io)
             full = np.zeros(self.n)
             full[v.dofs] = io
             term = Mv.matvec(full)
@@ -427,8 +445,12 @@ class OracleTissue:
         return np.where(self.frozen, self.act, -1.0)
 
 
-def pace_batch(model_name, P, u0, W0, dt, steps, order, n_stim, amp, t_end):
-    """0D splitting for many cells (ionic/__init__.py:140-163), cfg-1 oracle."""
+def pace_batch(model_name, P, u0, W0, dt, steps, order, n_stim, amp, t_end,
+               gate_scheme="bdf"):
+    """0D splitting for many cells (ionic/__init__.py:140-163), cfg-1 oracle.
+    gate_scheme="rush_larsen": order 1 with the Rush-Larsen state update."""
+    if gate_scheme == "rush_larsen":
+        assert order == 1
     n = u0.size
     uh, wh = [u0.copy()], [W0.copy()]
     peak = u0.copy()
@@ -441,7 +463,10 @@ def pace_batch(model_name, P, u0, W0, dt, steps, order, n_stim, amp, t_end):
         ue = OracleTissue._wsum(uh, _EXT[o])
         wb = OracleTissue._wsum(wh, _HIST[o])
         we = OracleTissue._wsum(wh, _EXT[o])
-        clamps += advance(model_name, ue, we, wb, _ALPHA[o], dt, P, W_out, I_out)
+        if gate_scheme == "rush_larsen":
+            clamps += advance_rl(model_name, ue, wh[0], dt, P, W_out, I_out)
+        else:
+            clamps += advance(model_name, ue, we, wb, _ALPHA[o], dt, P, W_out, I_out)
         t_next = (k + 1) * dt
         iapp = np.zeros(n)
         if t_next < t_end:

@@ -29,10 +29,12 @@ OP_DIASYM = 4
 DIA_MAX = 16
 ROW_SCRATCH = 1024        # MDX_ROW_SCRATCH
 MAX_LIFT = 8
-ABI_VERSION = 4   # include/mdx.h MDX_ABI_VERSION
+ABI_VERSION = 5   # include/mdx.h MDX_ABI_VERSION
+GATES_BDF, GATES_RUSH_LARSEN = 0, 1   # MDX_GATES_*
 
 STATUS_DIVERGED = 1
 STATUS_NONFINITE = 2
+STATUS_STOPPED = 4
 
 _p = C.c_void_p
 _i64 = C.c_int64
@@ -46,7 +48,7 @@ class TissueIonicArgs(C.Structure):
         ("w_ring", _p), ("ldw", _i64), ("ring_slots", _i32), ("head", _i32),
         ("order", _i32), ("prep", _i32), ("dt", _d), ("i_out", _p),
         ("clamp_count", _p), ("combo", _p), ("profiles", _p), ("ldp", _i64),
-        ("active_mask", C.c_uint64), ("n_impulses", _i32), ("_pad", _i32),
+        ("active_mask", C.c_uint64), ("n_impulses", _i32), ("gate_scheme", _i32),
         ("status", _p),
     ]
 
@@ -78,6 +80,8 @@ class CgArgs(C.Structure):
         ("row_out", _p), ("row_probes", _p), ("row_nprobes", _i32), ("_pad2", _i32),
         ("dom_row_host", _p), ("dom_m_row_host", _p),
         ("row_mask", _p), ("row_select", _i32), ("_pad3", _i32),
+        ("tstamps", _p), ("frozen_count", _p), ("frozen_target", _i64),
+        ("stop_when_full", _i32), ("_pad4", _i32),
     ]
 
 
@@ -108,7 +112,7 @@ class PaceArgs(C.Structure):
         ("n_stim_cells", _i64), ("period", _d), ("pulse_t0", _d * 8),
         ("pulse_dur", _d * 8), ("pulse_amp", _d * 8), ("n_trace_cells", _i64),
         ("trace_rows", _i64), ("stride", _i64), ("trace", _p),
-        ("clamp_count", _p), ("status", _p),
+        ("clamp_count", _p), ("status", _p), ("gate_scheme", _i32), ("_pad", _i32),
     ]
 
 
@@ -119,6 +123,8 @@ _SIGNATURES = {
     "mdx_ionic_num_params": ([C.c_int], C.c_int),
     "mdx_ionic_advance": ([C.c_int, _i64, _p, _p, _p, _i64, _i64, _d, _d, _p,
                            C.c_int, _p, _p, _p, _p], C.c_int),
+    "mdx_ionic_advance_rl": ([C.c_int, _i64, _p, _p, _i64, _i64, _d, _p, C.c_int, _p, _p,
+                              _p, _p], C.c_int),
     "mdx_ionic_current": ([C.c_int, _i64, _p, _p, _i64, _i64, _p, C.c_int, _p,
                            _p], C.c_int),
     "mdx_ionic_point_rates": ([C.c_int, _i64, _p, _p, _p, C.c_int, _p, _p, _p],

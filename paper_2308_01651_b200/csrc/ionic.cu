@@ -80,6 +80,31 @@ advance_strided(int64_t n, const double* __restrict__ u_ext,
   }
 }
 
+// Rush-Larsen one-step update (M::advance_rl) on strided state.
+template <class M>
+__global__ void __launch_bounds__(128)
+advance_rl_strided(int64_t n, const double* __restrict__ u, const double* __restrict__ W_n,
+                   int64_t cs, int64_t vs, double dt, const typename M::Params P,
+                   double* __restrict__ W_out, double* __restrict__ I_out,
+                   unsigned long long* clamp_count) {
+  int local_clamp = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double wn[M::NV], wo[M::NV];
+#pragma unroll
+    for (int v = 0; v < M::NV; ++v) wn[v] = W_n[i * cs + v * vs];
+    double I;
+    M::advance_rl(u[i], wn, dt, P, wo, I, local_clamp);
+#pragma unroll
+    for (int v = 0; v < M::NV; ++v) W_out[i * cs + v * vs] = wo[v];
+    I_out[i] = I;
+  }
+  if (clamp_count) {
+    int tot = __reduce_add_sync(0xffffffffu, local_clamp);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(clamp_count, (unsigned long long)tot);
+  }
+}
+
 template <class M>
 __global__ void __launch_bounds__(128)
 current_strided(int64_t n, const double* __restrict__ u, const double* __restrict__ W,
@@ -162,8 +187,10 @@ __device__ __forceinline__ double combine(const double (&x)[ORDER], const double
 // With `prep` set (single volume covering every DOF, identity map) it also
 // emits the RHS nodal term combo = u_BDF/dt + I_app and the CG warm start
 // x0 = u_EXT into the u ring's next slot, so no separate nodal pass runs.
+// RL (gate_scheme = MDX_GATES_RUSH_LARSEN): the states advance in one step from
+// W_n alone (M::advance_rl at u_EXT), so only the newest state slot is read.
 // ---------------------------------------------------------------------------
-template <class M, int ORDER>
+template <class M, int ORDER, bool RL>
 __global__ void __launch_bounds__(MDX_IONIC_BLOCK, MDX_IONIC_MINB)
 tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
   if (a.status && *(volatile const int32_t*)a.status) return;
@@ -193,8 +220,18 @@ tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
     const double u_ext = combine<ORDER>(uh, b.e);
 
     double I;
-    double we[M::NV], wb[M::NV], wo[M::NV];
-    {
+    double wo[M::NV];
+    if (RL) {
+      double wn[M::NV];
+      const double* p0 = wbase[0] + i;
+#pragma unroll
+      for (int v = 0; v < M::NV; ++v) {
+        wn[v] = *p0;
+        p0 += ldw;
+      }
+      M::advance_rl(u_ext, wn, a.dt, P, wo, I, local_clamp);
+    } else {
+      double we[M::NV], wb[M::NV];
       const double* p[ORDER];
 #pragma unroll
       for (int k = 0; k < ORDER; ++k) p[k] = wbase[k] + i;
@@ -209,8 +246,8 @@ tissue_ionic(mdx_tissue_ionic_args a, const typename M::Params P) {
         wb[v] = combine<ORDER>(wh, b.h);
         we[v] = M::NEEDS_WEXT ? combine<ORDER>(wh, b.e) : 0.0;
       }
+      M::advance(u_ext, we, wb, b.alpha, a.dt, P, wo, I, local_clamp);
     }
-    M::advance(u_ext, we, wb, b.alpha, a.dt, P, wo, I, local_clamp);
     {
       double* po = wout + i;
 #pragma unroll
@@ -282,7 +319,9 @@ tissue_prep(mdx_tissue_ionic_args a) {
 // state and BDF history in registers (pace_single_cell's splitting,
 // ionic/__init__.py:140-163, with t_{k+1} = (k+1)*dt).
 // ---------------------------------------------------------------------------
-template <class M, int ORDER>
+// RL: Rush-Larsen states (M::advance_rl from W_n at u_n) with the order-1
+// potential update u+ = u_n + dt (I_app - I_ion(u_n, W+)).
+template <class M, int ORDER, bool RL>
 __global__ void __launch_bounds__(128)
 pace_cells(mdx_pace_args a, const typename M::Params P) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -327,7 +366,8 @@ pace_cells(mdx_pace_args a, const typename M::Params P) {
       we[v] = se;
     }
     double I;
-    M::advance(ue, we, wb, b.alpha, a.dt, P, wo, I, nclamp);
+    if (RL) M::advance_rl(ue, wh[0], a.dt, P, wo, I, nclamp);
+    else M::advance(ue, we, wb, b.alpha, a.dt, P, wo, I, nclamp);
     const double t_next = (double)(k + 1) * a.dt;
     double iapp = 0.0;
     if (stim) {
@@ -466,6 +506,19 @@ static int advance_impl(int64_t n, const double* u, const double* We, const doub
 }
 
 template <class M>
+static int advance_rl_impl(int64_t n, const double* u, const double* Wn, int64_t cs,
+                           int64_t vs, double dt, const double* P, int np, double* Wo,
+                           double* Io, unsigned long long* clamp, cudaStream_t st) {
+  int err;
+  auto p = load_params<M>(P, np, &err);
+  if (err) return err;
+  if (n <= 0) return MDX_OK;
+  advance_rl_strided<M><<<grid_for(n, 128), 128, 0, st>>>(n, u, Wn, cs, vs, dt, p, Wo, Io,
+                                                          clamp);
+  return check_launch("mdx_ionic_advance_rl");
+}
+
+template <class M>
 static int current_impl(int64_t n, const double* u, const double* W, int64_t cs, int64_t vs,
                         const double* P, int np, double* Io, cudaStream_t st) {
   int err;
@@ -496,10 +549,24 @@ static int tissue_impl(const mdx_tissue_ionic_args* a, const double* P, int np,
   if (a->n <= 0) return MDX_OK;
   constexpr int B = MDX_IONIC_BLOCK;
   const int g = grid_for(a->n, B);
+  if (a->gate_scheme != MDX_GATES_BDF && a->gate_scheme != MDX_GATES_RUSH_LARSEN) {
+    set_error("gate scheme %d", a->gate_scheme);
+    return MDX_ERR_ARG;
+  }
+  const bool rl = a->gate_scheme == MDX_GATES_RUSH_LARSEN;
   switch (a->order) {
-    case 1: tissue_ionic<M, 1><<<g, B, 0, st>>>(*a, p); break;
-    case 2: tissue_ionic<M, 2><<<g, B, 0, st>>>(*a, p); break;
-    case 3: tissue_ionic<M, 3><<<g, B, 0, st>>>(*a, p); break;
+    case 1:
+      if (rl) tissue_ionic<M, 1, true><<<g, B, 0, st>>>(*a, p);
+      else tissue_ionic<M, 1, false><<<g, B, 0, st>>>(*a, p);
+      break;
+    case 2:
+      if (rl) tissue_ionic<M, 2, true><<<g, B, 0, st>>>(*a, p);
+      else tissue_ionic<M, 2, false><<<g, B, 0, st>>>(*a, p);
+      break;
+    case 3:
+      if (rl) tissue_ionic<M, 3, true><<<g, B, 0, st>>>(*a, p);
+      else tissue_ionic<M, 3, false><<<g, B, 0, st>>>(*a, p);
+      break;
     default: set_error("BDF order %d", a->order); return MDX_ERR_ARG;
   }
   return check_launch("mdx_tissue_ionic");
@@ -512,10 +579,22 @@ static int pace_impl(const mdx_pace_args* a, const double* P, int np, cudaStream
   if (err) return err;
   if (a->n_cells <= 0) return MDX_OK;
   const int g = (int)((a->n_cells + 127) / 128);
+  if (a->gate_scheme == MDX_GATES_RUSH_LARSEN) {
+    if (a->order != 1) {
+      set_error("Rush-Larsen pacing is a one-step scheme: order must be 1, got %d", a->order);
+      return MDX_ERR_ARG;
+    }
+    pace_cells<M, 1, true><<<g, 128, 0, st>>>(*a, p);
+    return check_launch("mdx_pace_cells");
+  }
+  if (a->gate_scheme != MDX_GATES_BDF) {
+    set_error("gate scheme %d", a->gate_scheme);
+    return MDX_ERR_ARG;
+  }
   switch (a->order) {
-    case 1: pace_cells<M, 1><<<g, 128, 0, st>>>(*a, p); break;
-    case 2: pace_cells<M, 2><<<g, 128, 0, st>>>(*a, p); break;
-    case 3: pace_cells<M, 3><<<g, 128, 0, st>>>(*a, p); break;
+    case 1: pace_cells<M, 1, false><<<g, 128, 0, st>>>(*a, p); break;
+    case 2: pace_cells<M, 2, false><<<g, 128, 0, st>>>(*a, p); break;
+    case 3: pace_cells<M, 3, false><<<g, 128, 0, st>>>(*a, p); break;
     default: set_error("BDF order %d", a->order); return MDX_ERR_ARG;
   }
   return check_launch("mdx_pace_cells");
@@ -563,6 +642,13 @@ int mdx_ionic_advance(int model, int64_t n, const double* u_ext, const double* W
                       unsigned long long* clamp_count, void* stream) {
   MDX_DISPATCH(model, (advance_impl<M>(n, u_ext, W_ext, W_bdf, cs, vs, alpha, dt, P, np,
                                        W_out, I_out, clamp_count, (cudaStream_t)stream)))
+}
+
+int mdx_ionic_advance_rl(int model, int64_t n, const double* u, const double* W_n, int64_t cs,
+                         int64_t vs, double dt, const double* P, int np, double* W_out,
+                         double* I_out, unsigned long long* clamp_count, void* stream) {
+  MDX_DISPATCH(model, (advance_rl_impl<M>(n, u, W_n, cs, vs, dt, P, np, W_out, I_out,
+                                          clamp_count, (cudaStream_t)stream)))
 }
 
 int mdx_ionic_current(int model, int64_t n, const double* u, const double* W, int64_t cs,

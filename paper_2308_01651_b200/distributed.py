@@ -358,7 +358,7 @@ class DistributedTissueSolver:
     PCG over the owned rows.
     """
 
-    def __init__(self, config, group=None, operator="auto", owner=None):
+    def __init__(self, config, group=None, operator="auto", owner=None, gate_scheme="bdf"):
         import torch
         import torch.distributed as dist
 
@@ -374,7 +374,8 @@ class DistributedTissueSolver:
         self.part = part
         self.n_global = mesh.nodes.shape[0]
         self.config = config
-        self.local = TissueSolver(local_config(config, part), operator=operator, cg_variant=2)
+        self.local = TissueSolver(local_config(config, part), operator=operator, cg_variant=2,
+                                  gate_scheme=gate_scheme)
         loc = self.local
         self.n_local = loc.n
         self.comm = HaloComm(part, group, device="cuda")

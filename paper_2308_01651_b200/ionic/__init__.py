@@ -79,9 +79,24 @@ def advance_ionic(spec, u_ext, w_ext, w_history, dt, scheme):
     return w_out[0]
 
 
+GATE_SCHEMES = {"bdf": N.GATES_BDF, "rush_larsen": N.GATES_RUSH_LARSEN}
+
+
+def gate_scheme_id(name):
+    """"bdf" (the reference's IMEX-BDF ionic update) or "rush_larsen" (exponential
+    gates + explicit Euler from W_n; BASELINE.json north_star / config 1)."""
+    try:
+        return GATE_SCHEMES[name]
+    except KeyError:
+        raise ValueError(f"gate_scheme must be one of {sorted(GATE_SCHEMES)}, got {name!r}")
+
+
 def pace_cells(spec, protocol, u0, W0, order=2, n_stim_cells=None,
-               trace_cells=0, stride=1, return_device=False):
+               trace_cells=0, stride=1, return_device=False, gate_scheme="bdf"):
     """Integrate many independent cells under one 0D protocol on the device.
+
+    gate_scheme="rush_larsen" is the one-step mode (order must be 1):
+    u+ = u_n + dt (I_app - I_ion(u_n, W+)).
 
     u0: (n,), W0: (n, nv) host arrays or CUDA tensors (SoA (nv, n) tensors
     are accepted too).  Cells [0, n_stim_cells) receive the protocol's
@@ -95,6 +110,9 @@ def pace_cells(spec, protocol, u0, W0, order=2, n_stim_cells=None,
         raise NotImplementedError(f"{spec.kind.value} has no kernels")
     nv = mod.NUM_VARS
     bdf_coefficients(order)
+    scheme_id = gate_scheme_id(gate_scheme)
+    if scheme_id == N.GATES_RUSH_LARSEN and order != 1:
+        raise ValueError("Rush-Larsen pacing is a one-step scheme: order must be 1")
     u = torch.as_tensor(np.asarray(u0, dtype=np.float64) if not
                         hasattr(u0, "is_cuda") else u0).to("cuda", torch.float64).contiguous().clone()
     n = u.shape[0]
@@ -134,6 +152,7 @@ def pace_cells(spec, protocol, u0, W0, order=2, n_stim_cells=None,
     a.trace = N.ptr(trace)
     a.clamp_count = N.ptr(clamp)
     a.status = N.ptr(status)
+    a.gate_scheme = scheme_id
     P = mod.pack(spec.parameters, spec.cell_type)
     Ph, Pp = N.host_doubles(P)
     N.check(N.lib().mdx_pace_cells(mod.MODEL_ID, N.C.byref(a), Pp, int(Ph.size),
@@ -147,10 +166,11 @@ def pace_cells(spec, protocol, u0, W0, order=2, n_stim_cells=None,
             peak.cpu().numpy(), int(clamp.item()), tr)
 
 
-def pace_single_cell(spec, protocol, order=2, stride=1):
+def pace_single_cell(spec, protocol, order=2, stride=1, gate_scheme="bdf"):
     """0D integration of one cell; returns (CellState, trace rows (t,u,w..))."""
     state = spec.initial_state
     u, W, _, _, trace = pace_cells(
         spec, protocol, np.array([float(state.u)]),
-        state.w.reshape(1, -1), order=order, trace_cells=1, stride=stride)
+        state.w.reshape(1, -1), order=order, trace_cells=1, stride=stride,
+        gate_scheme=gate_scheme)
     return CellState(float(u[0]), W[0].copy()), trace[0]

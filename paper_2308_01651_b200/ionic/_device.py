@@ -72,6 +72,33 @@ def advance(model_id, nv, u_ext, W_ext, W_bdf, alpha, dt, P, W_out, I_out):
     return int(clamp.item())
 
 
+def advance_rl(model_id, nv, u, W_n, dt, P, W_out, I_out):
+    """Rush-Larsen one-step update (`mdx_ionic_advance_rl`); returns the clamp count."""
+    torch = _torch()
+    lib = N.lib()
+    n = int(u.shape[0])
+    host_out = not _is_cuda_tensor(W_out)
+    u_d = _as_device(u, torch)
+    wn_d = _as_device(W_n, torch)
+    if host_out:
+        wo_d = torch.empty((n, nv), dtype=torch.float64, device="cuda")
+        io_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    else:
+        wo_d, io_d = W_out, I_out
+    cs, vs = _layout(wn_d, nv)
+    if _layout(wo_d, nv) != (cs, vs):
+        raise ValueError("W_n and W_out must share one layout")
+    clamp = torch.zeros(1, dtype=torch.int64, device="cuda")
+    Ph, Pp = N.host_doubles(P)
+    N.check(lib.mdx_ionic_advance_rl(
+        model_id, n, N.ptr(u_d), N.ptr(wn_d), cs, vs, float(dt), Pp, int(Ph.size),
+        N.ptr(wo_d), N.ptr(io_d), N.ptr(clamp), N.stream_handle()), "mdx_ionic_advance_rl")
+    if host_out:
+        W_out[...] = wo_d.cpu().numpy()
+        I_out[...] = io_d.cpu().numpy()
+    return int(clamp.item())
+
+
 def current(model_id, nv, u, W, P, I_out):
     torch = _torch()
     lib = N.lib()

@@ -97,6 +97,12 @@ def advance_kernel(u_ext, W_ext, W_bdf, alpha, dt, P, W_out, I_out):
                            P, W_out, I_out)
 
 
+def rush_larsen_kernel(u, W_n, dt, P, W_out, I_out):
+    """Rush-Larsen mode (not in the reference): gates exponential,
+    the rest explicit Euler, from W_n at potential u; I_out at (u, W_out)."""
+    return _device.advance_rl(MODEL_ID, NUM_VARS, u, W_n, dt, P, W_out, I_out)
+
+
 def current_kernel(u, W, P, I_out):
     _device.current(MODEL_ID, NUM_VARS, u, W, P, I_out)
 

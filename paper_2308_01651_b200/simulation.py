@@ -236,6 +236,14 @@ class SectionTimer:
     def device_span(self, name, start, end):
         self._events.append((name, start, end))
 
+    def device_stamps(self, stamps):
+        """`stamps`: CUDA int64 tensor (k, 4) of globaltimer ns written by the solve
+        kernels (mdx_cg_args.tstamps): start, assembly done, solve done, end."""
+        self._stamps = stamps
+
+    # the fused solve kernel's sections, from its own stamps
+    _STAMP_SECTIONS = ("Monodomain assembly", "Linear solver", "Other")
+
     @property
     def totals(self):
         out = dict(self._host)
@@ -243,6 +251,11 @@ class SectionTimer:
             self._events[-1][2].synchronize()
             for name, s, e in self._events:
                 out[name] += s.elapsed_time(e) * 1e-3
+        st = getattr(self, "_stamps", None)
+        if st is not None and st.numel():
+            d = (st[:, 1:] - st[:, :-1]).clamp_(min=0).sum(dim=0).cpu().numpy() * 1e-9
+            for name, v in zip(self._STAMP_SECTIONS, d):
+                out[name] += float(v)
         return out
 
 
@@ -297,9 +310,18 @@ def _pad(n):
 class TissueSolver:
     """Owns the device operators and state; advances the coupled system."""
 
-    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=None):
+    def __init__(self, config, operator="auto", blocks_hint=0, timed=False, cg_variant=None,
+                 gate_scheme="bdf"):
         validate_config(config)
         self.config = config
+        # "bdf": the reference's ionic update (advance_kernel).  "rush_larsen": the
+        # one-step mode of BASELINE.json's north_star (exponential gates, explicit
+        # Euler for the rest, from W_n at u_EXT) - not a reference scheme, checked
+        # against an oracle built from the reference's own gate/current functions.
+        from .ionic import gate_scheme_id
+
+        self.gate_scheme = gate_scheme
+        self._gate_scheme_id = gate_scheme_id(gate_scheme)
         self.timer = SectionTimer()
         self.timed = timed
         self.blocks_hint = blocks_hint
@@ -448,6 +470,13 @@ class TissueSolver:
         self.act_time = torch.full((n,), ACTIVATION_SENTINEL, **f64)
         self.best_slope = torch.full((n,), -np.inf, **f64)
         self.frozen = torch.from_numpy(inactive.astype(np.uint8)).cuda()
+        # device-side count of frozen nodes (inactive ones are frozen from the
+        # start) and the early-stop switch of run(stop_when_fully_activated=True)
+        self.frozen_count = torch.tensor([int(inactive.sum())], dtype=torch.int64,
+                                         device="cuda")
+        self.stop_when_full = False
+        self.stopped_at = None
+        self._stamp_log = None
 
         # solver workspace and logs
         from .linalg import CgWorkspace
@@ -491,7 +520,8 @@ class TissueSolver:
         base = dict(u_ring=N.ptr(self.u_ring), ldu=self.ld, ring_slots=RING_SLOTS,
                     dt=self.dt, clamp_count=N.ptr(self.clamps), combo=N.ptr(self.combo),
                     profiles=N.ptr(self.profiles), ldp=self.n,
-                    n_impulses=len(self._impulses), status=N.ptr(self.ws.status))
+                    n_impulses=len(self._impulses), status=N.ptr(self.ws.status),
+                    gate_scheme=self._gate_scheme_id)
         if not self.fused_prep:
             ia = N.TissueIonicArgs(**base)
             ia.n = self.n
@@ -522,6 +552,8 @@ class TissueSolver:
         a.act_time = N.ptr(self.act_time)
         a.best_slope = N.ptr(self.best_slope)
         a.frozen = N.ptr(self.frozen)
+        a.frozen_count = N.ptr(self.frozen_count)
+        a.frozen_target = self.n
         a.dt = self.dt
         a.tol = cfg.linear_solver.tolerance
         a.max_iter = cfg.linear_solver.max_iterations
@@ -589,7 +621,25 @@ class TissueSolver:
             self._log_ptrs = (self.iter_log.data_ptr(), self.relres_log.data_ptr())
         a.iters_out = self._log_ptrs[0] + 4 * slot
         a.relres_out = self._log_ptrs[1] + 8 * slot
+        a.stop_when_full = 1 if self.stop_when_full else 0
+        if self.timed:
+            a.tstamps = self._stamp_slot(slot)
         return a
+
+    def _stamp_slot(self, slot):
+        """Device address of this step's 4 section stamps (timed mode)."""
+        import torch
+
+        log = self._stamp_log
+        if log is None or slot >= log.shape[0]:
+            grow = max(1024, 2 * (slot + 1))
+            new = torch.zeros((grow, 4), dtype=torch.int64, device="cuda")
+            if log is not None:
+                new[: log.shape[0]] = log
+            self._stamp_log = log = new
+        self._stamp_used = max(getattr(self, "_stamp_used", 0), slot + 1)
+        self.timer.device_stamps(log[: self._stamp_used])
+        return log.data_ptr() + 32 * slot
 
     def enqueue_step(self, events=None, record=None):
         """Launch one step; no host synchronisation.
@@ -608,7 +658,7 @@ class TissueSolver:
         stream = self._stream
         timed = self.timed
         if timed:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             ev[0].record()
         self.enqueue_ionic(order, mask, head)
         if timed:
@@ -635,9 +685,9 @@ class TissueSolver:
         if events is not None:
             events[1].record()
         if timed:
-            ev[2].record()
+            # the ionic launches between two events; the solve kernel splits itself
+            # into assembly / solver / other through its section stamps
             self.timer.device_span("Ionic model update", ev[0], ev[1])
-            self.timer.device_span("Linear solver", ev[1], ev[2])
 
         self.advance_bookkeeping(head, nslot, t_next)
 
@@ -657,6 +707,9 @@ class TissueSolver:
 
         torch.cuda.current_stream().synchronize()
         st = int(self.ws.status.item())
+        if st == N.STATUS_STOPPED:
+            self._finish_stop()
+            return
         if self._pending:
             first = self._pending[0][0]
             last = self._pending[-1][0]
@@ -680,6 +733,24 @@ class TissueSolver:
                 raise SolverDivergence(-its, rel)
             raise NonFiniteSolution("linear solve produced non-finite entries")
         self._pending = []
+
+    def _finish_stop(self):
+        """Every node froze at step `fail_step` with stop_when_full set: the steps
+        enqueued after it were no-ops on the device; put the host bookkeeping back
+        to the state right after that step and clear the stop bit."""
+        stop = int(self.ws.fail_step.item())
+        first = self._pending[0][0] if self._pending else stop
+        its = self.iter_log[first - self._log_base: stop - self._log_base + 1]
+        if its.numel():
+            self._max_seen = max(self._max_seen, int(its.max().item()))
+            self._last_iters = int(its[-1].item())
+        for (k, head, t) in self._pending:
+            if k == stop + 1:            # the state before step stop+1 = after `stop`
+                self.step_index, self.head, self.time = k, head, t
+                break
+        self._pending = []
+        self.stopped_at = stop
+        self.ws.status.zero_()
 
     def step(self, return_potential=True):
         """Advance one step (TissueSolver.step, simulation.py:425-483).
@@ -739,8 +810,11 @@ class TissueSolver:
         return np.where(fr, self.act_time.cpu().numpy(), ACTIVATION_SENTINEL)
 
     def fully_activated(self):
-        fr = self.frozen.cpu().numpy().astype(bool)
-        return bool(fr[~self.inactive].all())
+        """Every conducting DOF has frozen its activation time (simulation.py:512):
+        one 8-byte read of the device-side counter the solve kernels maintain."""
+        if self.stopped_at is not None:
+            return True
+        return int(self.frozen_count.item()) >= self.n
 
     def record_row(self, probe_idx, dst):
         """Asynchronously copy [u_min, u_max, u[probes]] of the current
@@ -898,6 +972,8 @@ class TissueSolver:
         self.act_time.copy_(seg(act))
         self.best_slope.copy_(seg(best))
         self.frozen.copy_(seg(frozen).view(self.frozen.dtype))
+        self.frozen_count.copy_(self.frozen.ne(0).sum().view(1))
+        self.stopped_at = None
         self.step_index, self.time = int(step_index), float(t)
         self._log_base = self.step_index
         self.ws.status.zero_()
@@ -965,12 +1041,18 @@ def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
     n_rec = (n_steps - solver.step_index) // out.stride + 2
     pinned = torch.empty((n_rec, 2 + len(probes)), dtype=torch.float64, pin_memory=True)
     times = []
+    row_steps = []
+    # early stop on the device: the step that freezes the last node turns the
+    # steps enqueued after it into no-ops; the host looks every CHECK steps
+    solver.stop_when_full = bool(stop_when_fully_activated)
+    CHECK = 64
 
     def record():
         with solver.timer.section("Other"):
             if out.enable_csv or not out.enable_field_output:
                 solver.record_row(probe_idx, pinned[len(times)])   # async D2H
                 times.append(solver.time)
+                row_steps.append(solver.step_index)
             if out.enable_field_output:
                 path = f"{out.field_stem}_{solver.step_index:06d}.vtk"
                 write_vtk(path, config.mesh, {"transmembrane_potential": solver.potential})
@@ -986,15 +1068,25 @@ def run(config, stop_when_fully_activated=False, resume_from=None, **solver_kw):
             with solver.timer.section("Other"):
                 solver.enqueue_step(record=(probe_idx, pinned[len(times)]))
                 times.append(solver.time)
-            continue
-        solver.enqueue_step()
-        k = solver.step_index
-        if k % out.stride == 0 or k == n_steps:
-            record()
-        if stop_when_fully_activated and solver.fully_activated():
-            break
+                row_steps.append(solver.step_index)
+        else:
+            solver.enqueue_step()
+            k = solver.step_index
+            if k % out.stride == 0 or k == n_steps:
+                record()
+        if stop_when_fully_activated and (solver.step_index % CHECK == 0
+                                          or out.enable_field_output):
+            solver.sync()
+            if solver.stopped_at is not None:
+                break
     solver.sync()
-    rows = [(t, *pinned[i].tolist()) for i, t in enumerate(times)]
+    if solver.stopped_at is not None:
+        # rows of the no-op steps after the stop were never written
+        keep = [i for i, k in enumerate(row_steps) if k <= solver.step_index]
+        times = [times[i] for i in keep]
+        rows = [(t, *pinned[i].tolist()) for i, t in zip(keep, times)]
+    else:
+        rows = [(t, *pinned[i].tolist()) for i, t in enumerate(times)]
     with solver.timer.section("Other"):
         csv_path = None
         if out.enable_csv:

@@ -374,12 +374,190 @@ def cfg1_subset():
     np.savez_compressed(OUT / "cfg1_subset.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+# Rush-Larsen mode (BASELINE.json north_star / config 1; not a reference scheme,
+# SPEC.md:201).  The fixtures below replace ONLY the integrator: the targets,
+# currents and rates are the reference's own jitted functions
+# (ten_tusscher._gate_targets/_currents/_conc_rates/_total,
+# bueno_orovio._gate_pieces/_current, aliev_panfilov.advance_kernel), and the
+# tissue/0D drivers are the reference's TissueSolver / pace_single_cell at BDF
+# order 1 (where W_ext = W_bdf = W_n, alpha = 1) with <model>.advance_kernel
+# swapped for that integrator.
+# ---------------------------------------------------------------------------
+
+
+def _rl_kernels():
+    from numba import njit, prange
+
+    from monodomain.ionic import aliev_panfilov as ap
+    from monodomain.ionic import bueno_orovio as bo
+    from monodomain.ionic import ten_tusscher as tt
+
+    tt_targets, tt_currents, tt_conc, tt_total = (tt._gate_targets, tt._currents,
+                                                  tt._conc_rates, tt._total)
+    bo_pieces, bo_current = bo._gate_pieces, bo._current
+
+    @njit(parallel=True)
+    def ttp_rl(u, W_n, dt, P, W_out, I_out):
+        dt_ms = dt * 1.0e3
+        clamped = 0
+        for i in prange(u.shape[0]):
+            v = u[i] * 1.0e3
+            w = W_n[i]
+            targets = tt_targets(v, w[14], P[49])
+            nclamp = 0
+            for g in range(12):
+                inf = targets[2 * g]
+                gval = inf + (w[g] - inf) * np.exp(-dt_ms / targets[2 * g + 1])
+                if gval < 0.0:
+                    gval = 0.0
+                    nclamp += 1
+                elif gval > 1.0:
+                    gval = 1.0
+                    nclamp += 1
+                W_out[i, g] = gval
+            rates = tt_conc(w, tt_currents(v, w, P), P)
+            for c in range(6):
+                W_out[i, 12 + c] = w[12 + c] + dt_ms * rates[c]
+            I_out[i] = tt_total(tt_currents(v, W_out[i], P))
+            clamped += nclamp
+        return clamped
+
+    @njit(parallel=True)
+    def bo_rl(u, W_n, dt, P, W_out, I_out):
+        dt_ms = dt * 1.0e3
+        clamped = 0
+        for i in prange(u.shape[0]):
+            pieces = bo_pieces(u[i], P)
+            nclamp = 0
+            for g in range(3):
+                src, rate = pieces[2 * g], pieces[2 * g + 1]
+                inf = src / rate
+                gval = inf + (W_n[i, g] - inf) * np.exp(-dt_ms * rate)
+                if gval < 0.0:
+                    gval = 0.0
+                    nclamp += 1
+                elif gval > 1.0:
+                    gval = 1.0
+                    nclamp += 1
+                W_out[i, g] = gval
+            I_out[i] = bo_current(u[i], W_out[i, 0], W_out[i, 1], W_out[i, 2], P)
+            clamped += nclamp
+        return clamped
+
+    def apf_rl(u, W_n, dt, P, W_out, I_out):
+        return ap.advance_kernel(u, W_n, W_n, 1.0, dt, P, W_out, I_out)
+
+    return {"ttp06": (tt, ttp_rl), "bo": (bo, bo_rl), "apf": (ap, apf_rl)}
+
+
+class _RlPatch:
+    """Swap <module>.advance_kernel for the Rush-Larsen integrator (order-1 callers
+    pass W_ext = W_bdf = W_n and alpha = 1, checked)."""
+
+    def __init__(self, mod, rl):
+        self.mod, self.rl = mod, rl
+
+    def __enter__(self):
+        self.orig = self.mod.advance_kernel
+        rl = self.rl
+
+        def patched(u_ext, W_ext, W_bdf, alpha, dt, P, W_out, I_out):
+            assert alpha == 1.0 and np.array_equal(W_ext, W_bdf)
+            return rl(np.ascontiguousarray(u_ext), np.ascontiguousarray(W_bdf), dt, P,
+                      W_out, I_out)
+
+        self.mod.advance_kernel = patched
+        return self
+
+    def __exit__(self, *exc):
+        self.mod.advance_kernel = self.orig
+        return False
+
+
+def rl_kat():
+    """RL step on the ionic_kat inputs; cfg-1 subset in RL mode; 0D traces; two
+    small tissue runs (reference TissueSolver, BDF1, RL ionic update)."""
+    import dataclasses
+
+    from monodomain.ionic import (CellType, IonicModelSpec, ModelKind, PacingProtocol0D,
+                                  model_module, pace_single_cell)
+    from monodomain.simulation import TissueSolver
+
+    from paper_2308_01651_b200 import configs
+
+    K = _rl_kernels()
+    kat = np.load(OUT / "ionic_kat.npz")
+    out = {}
+    for tag, name in (("ttp06_epi", "ttp06"), ("ttp06_endo", "ttp06"), ("ttp06_myo", "ttp06"),
+                      ("bo_-", "bo"), ("apf_-", "apf")):
+        P, u, Wn = kat[f"{tag}_P"], kat[f"{tag}_u"], kat[f"{tag}_Wext"].copy()
+        if name != "apf":
+            ng = 12 if name == "ttp06" else 3
+            Wn[:16, :ng] = kat[f"{tag}_Wbdf"][:16, :ng]      # out-of-range gates: clamps
+        out[f"{tag}_Wn"] = Wn
+        for dt in ((2e-5, 1e-5) if name == "ttp06" else (5e-5, 1e-3)):
+            W_out, I_out = np.empty_like(Wn), np.empty(u.size)
+            c = K[name][1](u, Wn, dt, P, W_out, I_out)
+            out[f"{tag}_dt{dt:g}_Wout"] = W_out
+            out[f"{tag}_dt{dt:g}_Iout"] = I_out
+            out[f"{tag}_dt{dt:g}_clamped"] = np.array(c)
+    # config-1 subset, RL mode: u+ = u_n + dt (I_app - I_ion(u_n, W+))
+    n, steps, dt = 512, 2000, 1e-5
+    u, W = configs.config1_initial(n)
+    spec = IonicModelSpec(ModelKind.TTP06)
+    P = model_module(ModelKind.TTP06).pack(spec.parameters, spec.cell_type)
+    n_stim = n // 100
+    peak, clamps = u.copy(), 0
+    W_out, I_out = np.empty_like(W), np.empty(n)
+    for k in range(steps):
+        clamps += K["ttp06"][1](u, W, dt, P, W_out, I_out)
+        iapp = np.zeros(n)
+        if (k + 1) * dt < 1e-3:
+            iapp[:n_stim] = 52.0
+        u = (u + dt * (iapp - I_out)) / 1.0
+        W = W_out.copy()
+        peak = np.maximum(peak, u)
+    out.update(cfg1_u=u, cfg1_W=W, cfg1_peak=peak, cfg1_clamps=np.array(clamps),
+               cfg1_n_stim=np.array(n_stim))
+    # 0D traces through the reference's pace_single_cell at order 1
+    ttp = PacingProtocol0D((0.0,), (2e-3,), (35.714,), 0.0, 0.05, 2.5e-5)
+    with _RlPatch(*K["ttp06"]):
+        _, tr = pace_single_cell(IonicModelSpec(ModelKind.TTP06), ttp, order=1, stride=40)
+    out["ttp_trace"] = tr
+    bop = PacingProtocol0D((0.0,), (4e-3,), (1.1628e3,), 0.8, 0.4, 5e-5)
+    with _RlPatch(*K["bo"]):
+        _, tr = pace_single_cell(IonicModelSpec(ModelKind.BUENO_OROVIO), bop, order=1,
+                                 stride=20)
+    out["bo_trace"] = tr
+    # tissue: the reference solver at BDF1 with the RL ionic update
+    ns = configs.reference_namespace()
+    for key, name, cfg, steps in (
+            ("tissue_bo", "bo", configs.config0(ns), 400),
+            ("tissue_ttp", "ttp06", configs.config2(ns, h=0.5e-3), 1000)):
+        cfg = dataclasses.replace(cfg, bdf_order=1)
+        pts = configs.corner_probes() + [(10e-3, 3.5e-3, 1.5e-3)]
+        probes = [ns.nearest_node(cfg.mesh, p) for p in pts]
+        with _RlPatch(*K[name]):
+            solver = TissueSolver(cfg)
+            its, pr, umin, umax, _, _, wall = _drive(solver, steps, probes)
+        out[f"{key}_iters"] = its
+        out[f"{key}_probes"] = np.asarray(probes)
+        out[f"{key}_probe_u"] = pr
+        out[f"{key}_final_u"] = solver.potential
+        out[f"{key}_final_w"] = solver.volumes[0].ring[0]
+        out[f"{key}_activation"] = solver.activation_map
+        print(f"rl {key}: {steps} steps in {wall:.1f} s, iters {its.min()}..{its.max()}")
+    np.savez_compressed(OUT / "rl_kat.npz", **out)
+
+
 JOBS = {
     "ionic_kat": ionic_kat,
     "pace0d": pace0d,
     "operators": operators,
     "cg_kat": cg_kat,
     "cfg1_subset": cfg1_subset,
+    "rl_kat": rl_kat,
     "tissue_cfg0": lambda: tissue("tissue_cfg0", lambda c, ns: c.config0(ns), 800,
                                   snap_every=100, payload_at=(400,)),
     "tissue_ttp_h05": lambda: tissue("tissue_ttp_h05",

@@ -33,7 +33,7 @@ def header_functions():
 
 def test_header_declares_expected_entry_points():
     names = header_functions()
-    for must in ("mdx_ionic_advance", "mdx_ionic_current", "mdx_ionic_point_rates",
+    for must in ("mdx_ionic_advance", "mdx_ionic_advance_rl", "mdx_ionic_current", "mdx_ionic_point_rates",
                  "mdx_tissue_ionic", "mdx_tissue_prep", "mdx_pcg_solve", "mdx_spmv",
                  "mdx_assemble_local", "mdx_scatter_csr", "mdx_stencil_rows",
                  "mdx_pace_cells"):
@@ -55,7 +55,7 @@ def test_ctypes_binding_covers_header(built):
 
     assert set(header_functions()) == set(_native.EXPORTED_SYMBOLS)
     lib = _native.load_library(built)
-    assert lib.mdx_abi_version() == _native.ABI_VERSION == 4
+    assert lib.mdx_abi_version() == _native.ABI_VERSION == 5
     assert lib.mdx_ionic_num_vars(_native.MODEL_TTP06) == 18
     assert lib.mdx_ionic_num_vars(_native.MODEL_BUENO_OROVIO) == 3
     assert lib.mdx_ionic_num_vars(_native.MODEL_ALIEV_PANFILOV) == 1

@@ -179,3 +179,72 @@ def test_cfg1_batch_vs_reference_and_oracle(golden):
     ur, Wr, pr, _ = O.pace_batch("TTP06", P, u0, W0, 1e-5, 300, 2, 3, 52.0, 1e-3)
     np.testing.assert_allclose(u, ur, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(peak, pr, rtol=1e-9, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Rush-Larsen mode (gate_scheme="rush_larsen"; north_star / config 1).  Fixtures:
+# the reference's own gate/current/rate functions under the RL integrator
+# (tests/golden/make_golden.py: rl_kat).
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", ["ttp06_epi", "ttp06_endo", "ttp06_myo", "bo_-", "apf_-"])
+@pytest.mark.parametrize("layout", ["aos", "soa"])
+def test_rush_larsen_kernel_matches_reference_functions(golden, tag, layout):
+    import torch
+
+    g, kat = golden("rl_kat"), golden("ionic_kat")
+    mod = _module(tag)
+    u, P, Wn = kat[f"{tag}_u"], kat[f"{tag}_P"], g[f"{tag}_Wn"]
+    seen = 0
+    for key in g:
+        if not (key.startswith(f"{tag}_dt") and key.endswith("_Wout")):
+            continue
+        dt = float(key[len(tag) + 3: -len("_Wout")])
+        if layout == "aos":
+            Wo, Io = np.empty_like(Wn), np.empty(u.size)
+            c = mod.rush_larsen_kernel(u, Wn, dt, P, Wo, Io)
+        else:
+            wn_d = torch.from_numpy(np.ascontiguousarray(Wn.T)).cuda().t()
+            wo_d = torch.empty((Wn.shape[1], u.size), dtype=torch.float64, device="cuda").t()
+            io_d = torch.empty(u.size, dtype=torch.float64, device="cuda")
+            c = mod.rush_larsen_kernel(torch.from_numpy(u).cuda(), wn_d, dt, P, wo_d, io_d)
+            Wo, Io = wo_d.cpu().numpy(), io_d.cpu().numpy()
+        np.testing.assert_allclose(Wo, g[f"{tag}_dt{dt:g}_Wout"], rtol=1e-11, atol=1e-300)
+        np.testing.assert_allclose(Io, g[f"{tag}_dt{dt:g}_Iout"], rtol=1e-9, atol=1e-10)
+        assert c == int(g[f"{tag}_dt{dt:g}_clamped"])
+        seen += 1
+    assert seen == 2
+
+
+def test_rush_larsen_cfg1_subset_and_traces(golden):
+    """Config 1 as BASELINE words it (Rush-Larsen on gates): the 512-cell subset and
+    the 0D traces of the reference's pace_single_cell with the RL integrator."""
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.ionic import (IonicModelSpec, ModelKind, PacingProtocol0D,
+                                             pace_cells, pace_single_cell)
+
+    g = golden("rl_kat")
+    u0, W0 = configs.config1_initial(512)
+    spec = IonicModelSpec(ModelKind.TTP06)
+    proto = PacingProtocol0D((0.0,), (1e-3,), (52.0,), 0.0, 2000 * 1e-5, 1e-5)
+    u, W, peak, clamps, _ = pace_cells(spec, proto, u0, W0, order=1,
+                                       n_stim_cells=int(g["cfg1_n_stim"]),
+                                       gate_scheme="rush_larsen")
+    np.testing.assert_allclose(u, g["cfg1_u"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(peak, g["cfg1_peak"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(W, g["cfg1_W"], rtol=1e-6, atol=1e-12)
+    assert clamps == int(g["cfg1_clamps"])
+    with pytest.raises(ValueError):
+        pace_cells(spec, proto, u0, W0, order=2, gate_scheme="rush_larsen")
+    with pytest.raises(ValueError):
+        pace_cells(spec, proto, u0, W0, order=1, gate_scheme="euler")
+    ttp = PacingProtocol0D((0.0,), (2e-3,), (35.714,), 0.0, 0.05, 2.5e-5)
+    _, tr = pace_single_cell(spec, ttp, order=1, stride=40, gate_scheme="rush_larsen")
+    ref = g["ttp_trace"]
+    assert np.linalg.norm(tr[:, 1] - ref[:, 1]) / np.linalg.norm(ref[:, 1]) < 1e-9
+    bo = PacingProtocol0D((0.0,), (4e-3,), (1.1628e3,), 0.8, 0.4, 5e-5)
+    _, tr = pace_single_cell(IonicModelSpec(ModelKind.BUENO_OROVIO), bo, order=1, stride=20,
+                             gate_scheme="rush_larsen")
+    ref = g["bo_trace"]
+    assert np.linalg.norm(tr[:, 1] - ref[:, 1]) / np.linalg.norm(ref[:, 1]) < 1e-9

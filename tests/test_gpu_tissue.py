@@ -424,6 +424,150 @@ def test_cfg4_ventricle_100k_60ms(golden, ns):
     assert its.max() >= 20
 
 
+@pytest.mark.parametrize("key,steps", [("tissue_bo", 400), ("tissue_ttp", 1000)])
+def test_rush_larsen_tissue_vs_reference_functions(golden, ns, key, steps):
+    """gate_scheme="rush_larsen": the reference TissueSolver at BDF1 with its ionic
+    update swapped for the RL integrator over the reference's own gate/current/rate
+    functions (rl_kat golden) against the GPU solver in that mode."""
+    import dataclasses
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    g = golden("rl_kat")
+    cfg = configs.config0(ns) if key == "tissue_bo" else configs.config2(ns, h=0.5e-3)
+    dt = cfg.dt
+    s = TissueSolver(dataclasses.replace(cfg, bdf_order=1), gate_scheme="rush_larsen")
+    probes = g[f"{key}_probes"]
+    pu = np.empty((steps, probes.size))
+    for k in range(steps):
+        pu[k] = s.step()[probes]
+    its = s.iterations_log()
+    assert np.abs(its - g[f"{key}_iters"]).max() <= 1
+    assert _rel(pu, g[f"{key}_probe_u"]) < 1e-8
+    assert _rel(s.potential, g[f"{key}_final_u"]) < 1e-8
+    np.testing.assert_allclose(s.volume_state(0), g[f"{key}_final_w"], rtol=1e-6, atol=1e-10)
+    act, ref = s.activation_map, g[f"{key}_activation"]
+    assert np.array_equal(act >= 0, ref >= 0)
+    both = act >= 0
+    assert np.abs(act[both] - ref[both]).max() <= dt * (1 + 1e-9)
+    with pytest.raises(ValueError):
+        TissueSolver(cfg, gate_scheme="forward_euler")
+
+
+def test_rush_larsen_bdf2_potential_vs_oracle(ns):
+    """RL ionic update under the BDF2 potential (states from W_n, u at u_EXT): live
+    against the oracle in the same mode, three volumes."""
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = configs.config3(ns, h=0.5e-3)
+    s = TissueSolver(cfg, gate_scheme="rush_larsen")
+    o = O.OracleTissue(cfg, gate_scheme="rush_larsen")
+    for _ in range(300):
+        s.enqueue_step()
+        o.step()
+    s.sync()
+    assert np.abs(s.iterations_log() - np.array(o.iters)).max() <= 1
+    assert _rel(s.potential, o.potential) < 1e-9
+
+
+def test_five_section_device_timing(ns):
+    """timer.totals (simulation.py:225-254): with timed=True the ionic launches are
+    timed by CUDA events and the fused solve kernel splits itself into assembly /
+    solver / other through its globaltimer section stamps."""
+    import time
+
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TIMING_SECTIONS, TissueSolver
+
+    for build in (lambda: configs.config0(ns), lambda: configs.config0(ns, kind="Tet4")):
+        s = TissueSolver(build(), timed=True)
+        s.advance(5)
+        s.sync()
+        before = dict(s.timer.totals)
+        t0 = time.perf_counter()
+        s.advance(200)
+        s.sync()
+        wall = time.perf_counter() - t0
+        tot = s.timer.totals
+        assert tuple(tot) == TIMING_SECTIONS
+        d = {k: tot[k] - before[k] for k in tot}
+        for k in ("Ionic model update", "Monodomain assembly", "Linear solver"):
+            assert d[k] > 0.0, k
+        assert d["Other"] >= 0.0
+        dev = sum(d[k] for k in TIMING_SECTIONS[1:])
+        assert 0.3 * wall < dev < 1.05 * wall, (dev, wall)
+        assert d["Linear solver"] > d["Monodomain assembly"]      # CG 28-41 iterations
+
+
+def test_run_stops_on_device_when_fully_activated(ns):
+    """run(stop_when_fully_activated=True) (simulation.py:702-703; the reference
+    benchmark's mode, benchmark.py:166): the stop is detected on the device by the
+    step that freezes the last node - same step count as the oracle's per-step
+    check, no host synchronisation per step."""
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.simulation import TissueSolver, run
+
+    cfg = configs.config0(ns, final_time=60e-3)      # fully activated at step 1,045
+    o = O.OracleTissue(cfg)
+    n_steps = int(round(cfg.final_time / cfg.dt))
+    while o.step_index < n_steps:
+        o.step()
+        if o.frozen.all():
+            break
+    assert 100 < o.step_index < n_steps - 100          # it does stop early
+    rep = run(cfg, stop_when_fully_activated=True)
+    assert rep.steps == o.step_index
+    assert rep.solver.stopped_at == o.step_index - 1
+    assert rep.solver.time == pytest.approx(o.time, rel=1e-12)
+    assert _rel(rep.final_potential, o.potential) < 1e-9
+    assert (rep.activation_times >= 0).all()
+    assert np.abs(rep.activation_times - o.activation_map).max() <= cfg.dt * (1 + 1e-9)
+    assert rep.rows[-1][0] <= o.time + 1e-12 and len(rep.rows) >= 1
+    # the counter also answers fully_activated() without copying the frozen field
+    s = TissueSolver(cfg)
+    s.advance(50)
+    assert not s.fully_activated()
+    assert int(s.frozen_count.item()) == int(s.frozen.ne(0).sum().item())
+    s.restore(rep.solver.checkpoint_payload())
+    assert s.fully_activated()
+    # and the solver keeps stepping after a stop (status cleared)
+    rep.solver.stop_when_full = False
+    rep.solver.advance(3)
+    rep.solver.sync()
+    assert rep.solver.step_index == o.step_index + 3
+
+
+@pytest.mark.parametrize("build", ["cfg0", "ttp", "tet", "sell"])
+def test_solve_kernels_are_deterministic_run_to_run(ns, build):
+    """compute-sanitizer is closed on this GPU pool, so the custom grid barrier /
+    grid reduction (relaxed polling, double-buffered partials) is stress-checked
+    the other way: a race would show as run-to-run differences.  Two fresh solvers
+    must produce bit-identical potentials, states and iteration counts."""
+    from paper_2308_01651_b200 import configs, ventricle
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    def make():
+        if build == "cfg0":
+            return TissueSolver(configs.config0(ns))                 # resident, 3 blocks
+        if build == "ttp":
+            return TissueSolver(configs.config2(ns, h=0.25e-3))      # resident, many blocks
+        cfg = ventricle.config4(ns, *ventricle.size_for_nodes(60_000))
+        return TissueSolver(cfg, operator="auto" if build == "tet" else "sell")
+
+    outs = []
+    for _ in range(2):
+        s = make()
+        s.advance(150)
+        outs.append((s.potential, s.iterations_log(), s.volume_state(0)))
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][2], outs[1][2])
+
+
 def test_checkpoint_format_and_cross_restore(golden, ns):
     """Restore the REFERENCE's checkpoint (step 400) and continue to 800."""
     from paper_2308_01651_b200 import configs

@@ -190,3 +190,68 @@ def test_oracle_cfg4_ventricle_small(golden, ns):
     for _ in range(300):
         orc.step()
     assert np.array_equal(np.array(orc.iters), g["iters"][:300])
+
+
+# ---------------------------------------------------------------------------
+# Rush-Larsen mode: the oracle's integrator over the restated reference functions
+# against fixtures built from the reference's OWN jitted functions with the same
+# integrator (tests/golden/make_golden.py: rl_kat)
+# ---------------------------------------------------------------------------
+
+RL_CASES = [("ttp06_epi", "TTP06"), ("ttp06_endo", "TTP06"), ("ttp06_myo", "TTP06"),
+            ("bo_-", "Bueno-Orovio"), ("apf_-", "Aliev-Panfilov")]
+
+
+@pytest.mark.parametrize("tag,model", RL_CASES)
+def test_oracle_rush_larsen_step(golden, tag, model):
+    g, kat = golden("rl_kat"), golden("ionic_kat")
+    u, P, Wn = kat[f"{tag}_u"], kat[f"{tag}_P"], g[f"{tag}_Wn"]
+    seen = 0
+    for key in g:
+        if key.startswith(f"{tag}_dt") and key.endswith("_Wout"):
+            dt = float(key[len(tag) + 3: -len("_Wout")])
+            Wo, Io = np.empty_like(Wn), np.empty(u.size)
+            c = O.advance_rl(model, u, Wn, dt, P, Wo, Io)
+            np.testing.assert_allclose(Wo, g[f"{tag}_dt{dt:g}_Wout"], rtol=1e-13, atol=1e-300)
+            np.testing.assert_allclose(Io, g[f"{tag}_dt{dt:g}_Iout"], rtol=1e-11, atol=1e-12)
+            assert c == int(g[f"{tag}_dt{dt:g}_clamped"])
+            if model != "Aliev-Panfilov":
+                assert c > 0                      # the out-of-range gates were clamped
+            seen += 1
+    assert seen == 2
+
+
+def test_oracle_rush_larsen_cfg1_subset(golden):
+    from paper_2308_01651_b200 import configs
+    from paper_2308_01651_b200.ionic import ten_tusscher as T
+
+    g = golden("rl_kat")
+    u0, W0 = configs.config1_initial(512)
+    P = T.pack(T.default_parameters())
+    u, W, peak, clamps = O.pace_batch("TTP06", P, u0, W0, 1e-5, 2000, 1, int(g["cfg1_n_stim"]),
+                                      52.0, 1e-3, gate_scheme="rush_larsen")
+    np.testing.assert_allclose(u, g["cfg1_u"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(W, g["cfg1_W"], rtol=1e-8, atol=1e-14)
+    np.testing.assert_allclose(peak, g["cfg1_peak"], rtol=1e-9, atol=1e-12)
+    assert clamps == int(g["cfg1_clamps"])
+
+
+@pytest.mark.parametrize("key,steps", [("tissue_bo", 400), ("tissue_ttp", 1000)])
+def test_oracle_rush_larsen_tissue(golden, ns, key, steps):
+    """Reference TissueSolver at BDF1 with the RL ionic update vs the oracle in
+    gate_scheme="rush_larsen" mode: same iterations, probes, activation map."""
+    import dataclasses
+
+    from paper_2308_01651_b200 import configs
+
+    g = golden("rl_kat")
+    cfg = configs.config0(ns) if key == "tissue_bo" else configs.config2(ns, h=0.5e-3)
+    orc = O.OracleTissue(dataclasses.replace(cfg, bdf_order=1), gate_scheme="rush_larsen")
+    probes = g[f"{key}_probes"]
+    pu = np.empty((steps, probes.size))
+    for k in range(steps):
+        pu[k] = orc.step()[probes]
+    assert np.array_equal(np.array(orc.iters), g[f"{key}_iters"])
+    np.testing.assert_allclose(pu, g[f"{key}_probe_u"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(orc.potential, g[f"{key}_final_u"], rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(orc.activation_map, g[f"{key}_activation"])
