@@ -314,9 +314,15 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("MDX_BENCH_DIST") == "1":
+        # MDX_BENCH_DIST=1: the partitioned solver at one rank (a one-GPU pool can
+        # still time its per-iteration phase path against the single-GPU kernel)
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return run_distributed(args, rank, world, local, dist)
 
@@ -442,6 +448,8 @@ def run_distributed(args, rank, world, local, dist):
     solver = DistributedTissueSolver(cfg)
     while solver.step_index < max(args.warmup, wl["window"]):
         solver.step()
+    # the window's start state, kept in pinned host memory for the e2e leg
+    snap = solver.snapshot_host()
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = solver.launches
@@ -461,9 +469,8 @@ def run_distributed(args, rank, world, local, dist):
     launches = solver.launches - launches0
 
     # e2e: every rank re-uploads its window-start state from pinned host
-    # memory, runs the same K steps through step() and reads each step's
-    # local potential range back to the host
-    snap = solver.snapshot_host()
+    # memory (the snapshot taken before the timed loop), runs the SAME K steps
+    # through step() and reads each step's local potential range back to the host
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -475,6 +482,7 @@ def run_distributed(args, rank, world, local, dist):
     torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
     dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+    e2e_its = np.array(solver.iters[-args.steps:])
     if rank == 0:
         line = {
             "metric": wl["metric"], "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
@@ -489,7 +497,8 @@ def run_distributed(args, rank, world, local, dist):
             "gpu_launches": launches,
             "e2e": {"value": n * args.steps / float(wall.item()), "unit": UNIT,
                     "h2d_bytes_per_step": h2d * world / args.steps,
-                    "d2h_bytes_per_step": 16 * world},
+                    "d2h_bytes_per_step": 16 * world,
+                    "same_steps_as_value": bool(np.array_equal(e2e_its, its))},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -43,7 +43,7 @@ def build(force=False, verbose=False, ptxas_info=False):
     nvcc = nvcc_path()
     BUILD.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "mdx.h"]
-    objs = []
+    objs, jobs = [], []
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
@@ -52,13 +52,23 @@ def build(force=False, verbose=False, ptxas_info=False):
                    "-c", str(src), "-o", str(obj)]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
-            if verbose:
-                print(" ".join(cmd), file=sys.stderr)
-            res = subprocess.run(cmd, capture_output=True, text=True)
-            if res.returncode != 0:
-                raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
-            if ptxas_info or verbose:
-                print(res.stderr, file=sys.stderr)
+            jobs.append((src, cmd))
+
+    def compile_one(job):
+        src, cmd = job
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
+        if ptxas_info or verbose:
+            print(res.stderr, file=sys.stderr)
+
+    if jobs:       # the translation units are independent: compile them side by side
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+            list(pool.map(compile_one, jobs))
     if force or _stale(LIB, objs):
         cmd = [nvcc, *ARCH, "-shared", "-cudart", "static",
                *[str(o) for o in objs], "-o", str(LIB)]
