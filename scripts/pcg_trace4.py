@@ -36,6 +36,9 @@ def main():
     t0 = t[:, 0, 0].min()
     arrive, release = (t[:, :, 0] - t0) / 1e3, (t[:, :, 1] - t0) / 1e3
     print(f"n {s.n} blocks {nb} traced reductions {ne} CG iterations {its}")
+    out = Path(__file__).resolve().parents[1] / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    np.savez_compressed(out / "trace_cfg4.npz", arrive=arrive, release=release)
     print(f"kernel span to last traced event {release.max():.1f} us")
     # event 0: RHS/r0 pass; then per iteration (Q event, R event)
     ph = arrive[:, 1:] - release[:, :-1]
