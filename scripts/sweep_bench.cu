@@ -118,6 +118,38 @@ sweepQ_tile(Dia op, const double* __restrict__ vals, const double* p, double* __
   if (s0 == 123.456) out[0] = s0;
 }
 
+// theta-strips marched along phi: the block's rows of consecutive planes sit one
+// plane (nx*nth rows) apart, so the phi-neighbours' p values and the mirrored
+// coefficients of the previous plane are still in L1 when the next plane needs them
+struct Strips { int nx, nth, nph, S; int th0[40]; long unit0[700]; };   // unit0: per-block first unit
+
+template <int NPT, int BLK, int MINB>
+__global__ void __launch_bounds__(BLK, MINB)
+sweepQ_strip(Dia op, Strips g, const double* __restrict__ vals, const double* p,
+             double* __restrict__ q, double* out) {
+  double s0 = 0;
+  const long u0 = g.unit0[blockIdx.x], u1 = g.unit0[blockIdx.x + 1];
+  const long plane = (long)g.nx * g.nth;
+  for (long u = u0; u < u1; u += NPT) {
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      const long uu = u + k;
+      if (uu < u1) {
+        const int s = (int)(uu / g.nph), ph = (int)(uu % g.nph);
+        const int t0 = g.th0[s], rows = g.nx * (g.th0[s + 1] - t0);
+        const long base = (long)g.nx * t0 + plane * ph;
+        for (int r = threadIdx.x; r < rows; r += BLK) {
+          const long i = base + r;
+          const double qi = dia_row(op, vals, p, i);
+          q[i] = qi;
+          s0 = fma(p[i], qi, s0);
+        }
+      }
+    }
+  }
+  if (s0 == 123.456) out[0] = s0;
+}
+
 __global__ void fill(double* a, long n, double v) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     a[i] = v * (1.0 + 1e-3 * (i % 977));
@@ -139,7 +171,7 @@ float timeit(F f, int reps = 20) {
 int main() {
   const long n = 10276240;
   Dia op; op.n = n; op.ld = n;
-  const long nx = 41, nxy = 41 * 240;
+  const long nx = 41, nxy = 41 * 241;
   const long offs[NP] = {1, nx, nx + 1, nxy, nxy + 1, nxy + nx, nxy + nx + 1};
   for (int s = 0; s < NP; ++s) op.off[s] = offs[s];
   double *vals, *r, *p, *q, *x, *dinv, *out;
@@ -155,7 +187,7 @@ int main() {
   const double GB = 1e-9 * n;
   float ms;
   printf("SMs %d\n", sms);
-  for (int g : {sms * 2, sms * 4, sms * 8, 20071}) {
+  for (int g : {sms * 2}) {
     ms = timeit([&] { sweepP<4><<<g, 512>>>(n, r, dinv, p, x, 1e-9, 0.5); });
     printf("P  npt4 grid %6d: %.3f ms  %.0f GB/s (48 B)\n", g, ms, 48 * GB / (ms * 1e-3));
     ms = timeit([&] { sweepR<4><<<g, 512>>>(n, r, q, dinv, 1e-9, out); });
@@ -174,6 +206,34 @@ int main() {
     printf("Qt npt4 b512 grid %6d: %.3f ms  %.0f GB/s\n", g, ms, 80 * GB / (ms * 1e-3));
     ms = timeit([&] { sweepQ_tile<2, 256, 6><<<g * 3, 256>>>(op, vals, p, q, out); });
     printf("Qt npt2 b256x6 grid %6d: %.3f ms  %.0f GB/s\n", g * 3, ms, 80 * GB / (ms * 1e-3));
+  }
+  for (int S : {21, 31, 16, 41}) {
+    for (int G : {sms * 2, sms * 4}) {
+      Strips g; g.nx = 41; g.nth = 241; g.nph = 1040; g.S = S;
+      for (int k = 0; k <= S; ++k) g.th0[k] = (int)((long)k * g.nth / S);
+      // units (strip-major, phi) split over the blocks at equal cumulative rows
+      std::vector<long> cum((size_t)S * g.nph + 1, 0);
+      for (long u = 0; u < (long)S * g.nph; ++u)
+        cum[u + 1] = cum[u] + g.nx * (g.th0[u / g.nph + 1] - g.th0[u / g.nph]);
+      long u = 0;
+      for (int b = 0; b <= G; ++b) {
+        const long target = cum.back() * b / G;
+        while (u < (long)S * g.nph && cum[u] < target) ++u;
+        g.unit0[b] = u;
+      }
+      g.unit0[G] = (long)S * g.nph;
+      if (G == sms * 2) {
+        ms = timeit([&] { sweepQ_strip<1, 512, 2><<<G, 512>>>(op, g, vals, p, q, out); });
+        printf("Qs S=%d npt1 b512 grid %d: %.3f ms  %.0f GB/s\n", S, G, ms, 80 * GB / (ms * 1e-3));
+        ms = timeit([&] { sweepQ_strip<2, 512, 2><<<G, 512>>>(op, g, vals, p, q, out); });
+        printf("Qs S=%d npt2 b512 grid %d: %.3f ms  %.0f GB/s\n", S, G, ms, 80 * GB / (ms * 1e-3));
+      } else {
+        ms = timeit([&] { sweepQ_strip<1, 256, 4><<<G, 256>>>(op, g, vals, p, q, out); });
+        printf("Qs S=%d npt1 b256x4 grid %d: %.3f ms  %.0f GB/s\n", S, G, ms, 80 * GB / (ms * 1e-3));
+        ms = timeit([&] { sweepQ_strip<2, 256, 4><<<G, 256>>>(op, g, vals, p, q, out); });
+        printf("Qs S=%d npt2 b256x4 grid %d: %.3f ms  %.0f GB/s\n", S, G, ms, 80 * GB / (ms * 1e-3));
+      }
+    }
   }
   // the whole iteration back to back (L2 carry-over between sweeps)
   ms = timeit([&] {

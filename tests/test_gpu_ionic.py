@@ -248,3 +248,51 @@ def test_rush_larsen_cfg1_subset_and_traces(golden):
                              gate_scheme="rush_larsen")
     ref = g["bo_trace"]
     assert np.linalg.norm(tr[:, 1] - ref[:, 1]) / np.linalg.norm(ref[:, 1]) < 1e-9
+
+
+def test_empty_and_ragged_inputs_through_the_abi():
+    """Edge cases at the C-ABI: zero-length batches are no-ops that return MDX_OK
+    (the reference's prange kernels accept empty arrays), a batch that is not a
+    multiple of the block or warp size is handled to the last cell, a wrong
+    parameter count is refused with a message, and a non-finite state is reported."""
+    import torch
+
+    from paper_2308_01651_b200 import _native as N
+    from paper_2308_01651_b200.errors import NonFiniteState
+    from paper_2308_01651_b200.ionic import (IonicModelSpec, ModelKind, PacingProtocol0D,
+                                             pace_cells, ten_tusscher as T)
+
+    lib = N.lib()
+    spec = IonicModelSpec(ModelKind.TTP06)
+    P = T.pack(spec.parameters)
+    Ph, Pp = N.host_doubles(P)
+    st = N.stream_handle()
+    assert lib.mdx_ionic_advance(N.MODEL_TTP06, 0, None, None, None, 18, 1, 1.0, 1e-5, Pp,
+                                 int(Ph.size), None, None, None, st) == 0
+    assert lib.mdx_ionic_advance_rl(N.MODEL_TTP06, 0, None, None, 18, 1, 1e-5, Pp, int(Ph.size),
+                                    None, None, None, st) == 0
+    assert lib.mdx_ionic_current(N.MODEL_TTP06, 0, None, None, 18, 1, Pp, int(Ph.size), None,
+                                 st) == 0
+    assert lib.mdx_record_row(None, 0, None, 0, None, None, st) == 0
+    # wrong packed-parameter length: refused, with the reason in mdx_last_error
+    assert lib.mdx_ionic_advance(N.MODEL_TTP06, 1, None, None, None, 18, 1, 1.0, 1e-5, Pp, 7,
+                                 None, None, None, st) != 0
+    assert b"50" in lib.mdx_last_error()
+    assert lib.mdx_ionic_advance(99, 1, None, None, None, 18, 1, 1.0, 1e-5, Pp, int(Ph.size),
+                                 None, None, None, st) != 0
+    # ragged batch sizes: every cell equals the single-cell result
+    st0 = spec.initial_state
+    proto = PacingProtocol0D((0.0,), (1e-3,), (52.0,), 0.0, 50e-5, 1e-5)
+    for n in (1, 31, 33, 129, 1000):
+        u0 = np.full(n, st0.u)
+        W0 = np.tile(st0.w, (n, 1))
+        u, W, peak, _, _ = pace_cells(spec, proto, u0, W0, order=2)
+        assert u.shape == (n,) and W.shape == (n, 18)
+        assert np.all(u == u[0]) and np.all(W == W[0])
+    u, W, _, _, _ = pace_cells(spec, proto, np.empty(0), np.empty((0, 18)), order=2)
+    assert u.size == 0 and W.shape == (0, 18)
+    bad = np.tile(st0.w, (4, 1))
+    bad[2, 12] = np.nan                      # Cai of one cell
+    with pytest.raises(NonFiniteState):
+        pace_cells(spec, proto, np.full(4, st0.u), bad, order=2)
+    torch.cuda.synchronize()
