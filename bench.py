@@ -227,6 +227,66 @@ def cpu_sample(name, steps, warmup=2):
                 iters=orc.iters[max(2, warmup):], setup=setup, n=n)
 
 
+def cpu_probe(kind):
+    """Child process of `cpu_extras`: config 2 (442,401-node slab) on the host CPU,
+    2 untimed start-up steps then 8 timed ones; prints one JSON object.
+    kind "port1": the oracle port on ONE thread (OMP_NUM_THREADS=1 in the child's
+    environment).  kind "numba": the UNMODIFIED reference package from baseline/_ref
+    (Python + numba, all threads) through its own TissueSolver.step."""
+    from paper_2308_01651_b200 import configs
+
+    steps = 8
+    if kind == "numba":
+        sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+        import numba
+        from monodomain.simulation import TissueSolver as RefSolver
+
+        cfg = configs.config2(configs.reference_namespace())
+        solver = RefSolver(cfg)
+        step, threads = solver.step, numba.get_num_threads()
+        iters = lambda: solver.last_iterations          # noqa: E731
+    else:
+        from oracle import monodomain_oracle as O
+
+        cfg = configs.config2(configs.this_package())
+        solver = O.OracleTissue(cfg)
+        step, threads = solver.step, O.num_threads()
+        iters = lambda: solver.iters[-1]                # noqa: E731
+    for _ in range(2):
+        step()
+    its = []
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+        its.append(int(iters()))
+    wall = time.perf_counter() - t0
+    n = cfg.mesh.nodes.shape[0]
+    print(json.dumps({"value": n * steps / wall, "unit": UNIT, "cores": threads,
+                      "sample": f"config 2 ({n} nodes), {steps} steps after 2 start-up steps "
+                                f"from rest (CG {min(its)}..{max(its)})"}), flush=True)
+
+
+def cpu_extras():
+    """Two more CPU numbers on config 2 (all cores and one thread; the
+    reference's own numba path): bounded to ~a minute, failures reported in place."""
+    out = {}
+    for key, kind, env in (("port_one_thread_cfg2", "port1", {"OMP_NUM_THREADS": "1"}),
+                           ("reference_numba_cfg2", "numba",
+                            {"NUMBA_CACHE_DIR": "/tmp/numba_cache_mdx"})):
+        if kind == "numba" and not (ROOT / "baseline" / "_ref" / "monodomain").is_dir():
+            out[key] = {"unavailable": "baseline/_ref not installed"}
+            continue
+        try:
+            res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-probe", kind],
+                                 env={**os.environ, **env}, capture_output=True, text=True,
+                                 timeout=240)
+            out[key] = json.loads(res.stdout.strip().splitlines()[-1])
+            out[key]["kind"] = "reference" if kind == "numba" else "port"
+        except Exception as exc:                       # noqa: BLE001
+            out[key] = {"unavailable": f"{type(exc).__name__}: {str(exc)[:120]}"}
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -432,6 +492,7 @@ def run_ours(args):
             "value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
             "sample": f"oracle port, {r['steps']} full step(s) of the same mesh after the 2 "
                       f"BDF start-up steps from rest (CG {min(r['iters'])}..{max(r['iters'])})"}
+        line["cpu_baseline"].update(cpu_extras())
     print(json.dumps(line), flush=True)
 
 
@@ -524,7 +585,11 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-probe", default=None, choices=["port1", "numba"],
+                    help="internal: child process of the cpu_baseline extras")
     args = ap.parse_args()
+    if args.cpu_probe:
+        return cpu_probe(args.cpu_probe)
     if args.warmup < 3:
         args.warmup = 3
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
