@@ -902,6 +902,28 @@ def test_stream_kernel_parity(tmp_path):
     assert m and int(m.group(1)) >= 3 and " failed" not in out, out[-2000:]
 
 
+def test_tiny_meshes_cooperative_grid_path(tmp_path):
+    """Meshes of <= 6,144 nodes run the resident PCG as one thread-block cluster with
+    DSMEM reductions (the default: the config-0 and h=0.5 mm TTP06 goldens above go
+    through it with 6 blocks, smoke() with 2).
+    MDX_PCG_CLUSTER=0 (chosen once per process) keeps the cooperative-grid reduction:
+    the same goldens in a child pytest, and a launch-plan line to prove the switch."""
+    import os
+    import re
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MDX_PCG_CLUSTER="0")
+    sel = "cfg0_bo_full_run or rush_larsen_tissue_vs_reference_functions or fused_output_row"
+    res = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-k", sel,
+                          "-p", "no:cacheprovider", __file__],
+                         env=env, capture_output=True, text=True, timeout=900)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    m = re.search(r"(\d+) passed", out)
+    assert m and int(m.group(1)) >= 3 and " failed" not in out, out[-2000:]
+
+
 def test_restore_from_pinned_tensor(ns):
     """restore() from a pinned uint8 tensor (one async DMA) = restore from bytes."""
     import torch
