@@ -64,6 +64,8 @@ def main():
           f"device {ms / args.steps:.3f} ms/step host {wall / args.steps * 1e3:.3f} ms/step "
           f"iters {its.min()}..{its.max()} mean {its.mean():.2f} "
           f"DoF*steps/s {s.n * args.steps / (ms * 1e-3):.3e}")
+    if args.steps <= 16:
+        print("iterations of every step since rest:", s.iterations_log().tolist())
 
 
 if __name__ == "__main__":

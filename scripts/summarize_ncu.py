@@ -2,9 +2,11 @@
 
     python scripts/summarize_ncu.py <out.md> <launches.csv> <rep1> [<rep2> ...]
                                     [--n KERNEL_SUBSTRING=ROWS ...]
+                                    [--iters KERNEL_SUBSTRING=K ...]
 
---n records how many nodes/DOFs the captured launch processed, so bench.py can
-scale the per-launch DRAM bytes to its own launch size.
+--n records how many nodes/DOFs the captured launch processed, and --iters how many
+CG iterations it ran, so bench.py can scale the per-launch DRAM bytes to its own
+launch size and iteration count.
 """
 import csv
 import io
@@ -104,6 +106,12 @@ def main():
         k, v = argv[i + 1].split("=")
         sizes[k] = int(float(v))
         del argv[i:i + 2]
+    iters = {}
+    while "--iters" in argv:
+        i = argv.index("--iters")
+        k, v = argv[i + 1].split("=")
+        iters[k] = int(v)
+        del argv[i:i + 2]
     out, launches, reps = argv[0], argv[1], argv[2:]
     lines = ["# ncu summary", ""]
     traffic = {}
@@ -122,6 +130,9 @@ def main():
             for k, v in sizes.items():
                 if k in name:
                     entry["n"] = v
+            for k, v in iters.items():
+                if k in name:
+                    entry["cg_iterations"] = v
             traffic[name.split("(")[0]] = entry
         except (KeyError, ValueError):
             pass
