@@ -271,3 +271,5 @@ def test_dia_layout_ventricle_seam():
     ptr = op.rem_ptr.numpy()
     for c in range(ptr.size - 1):
         assert np.all(rr[ptr[c]:ptr[c + 1]] // 32 == c)
+    # sorted by row: the kernels find a row's entries by a lower-bound search
+    assert np.all(np.diff(rr) >= 0)
