@@ -435,7 +435,9 @@ def run_ours(args):
     pcg_ach = float(sb.sum() / (solve_ms.sum() * 1e-3) / 1e9)
     ion_ach = ib / ionic_s / 1e9
     step_ach = float((sb + ib).sum() / (ms * 1e-3) / 1e9)
-    kname = {4: f"pcg_kernel<DIASYM{solver.op.np_},tissue,NPT> (reference CG recurrences)",
+    recur = {0: "reference CG recurrences, 3 sweeps", 1: "reference CG with q = A z + beta q, 2 sweeps",
+             2: "pipelined PCG, 1 sweep"}[solver.cg_variant]
+    kname = {4: f"pcg_kernel<DIASYM{solver.op.np_},tissue,NPT> ({recur})",
              3: "pcg_kernel<SELL>", 2: "pcg_kernel<CSR>",
              1: "pcg_resident_kernel<tissue>"}[solver.op.kind]
     t_pcg = traffic_of("pcg_kernel" if solver.op.kind != 1 else "pcg_resident_kernel")
