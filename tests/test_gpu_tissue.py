@@ -683,13 +683,19 @@ def _dist_cfg(name):
     return ventricle.config4(ns, n_xi=4, n_th=24, n_ph=64, final_time=30e-3)
 
 
-@pytest.mark.parametrize("name,steps", [("tissue_cfg0", 300), ("tissue_cfg4_small", 500)])
-def test_distributed_solver_single_rank_on_gpu(golden, name, steps):
+@pytest.mark.parametrize("name,steps,sweep_min", [("tissue_cfg0", 300, None),
+                                                  ("tissue_cfg4_small", 500, None),
+                                                  ("tissue_cfg4_small", 500, 1)])
+def test_distributed_solver_single_rank_on_gpu(golden, monkeypatch, name, steps, sweep_min):
     """DistributedTissueSolver (rank-local TissueSolver, phase kernels with
     row classes, NCCL plumbing) with one rank reproduces the reference run
-    (multi-rank host logic: tests/test_distributed.py over gloo)."""
+    (multi-rank host logic: tests/test_distributed.py over gloo).  sweep_min=1
+    runs the large-slab sweep kernel (pcg_sweep_kernel) on the small mesh."""
     import os
     import socket
+
+    if sweep_min is not None:
+        monkeypatch.setenv("MDX_SWEEP_MIN_ROWS", str(sweep_min))
 
     import torch.distributed as dist
 
@@ -737,9 +743,11 @@ def _gloo_gpu_worker(rank, world, port, name, steps, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,steps,kind", [("tissue_cfg0", 200, 1),
-                                             ("tissue_cfg4_small", 500, 4)])
-def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path, name, steps, kind):
+@pytest.mark.parametrize("name,steps,kind,sweep_min", [("tissue_cfg0", 200, 1, None),
+                                                       ("tissue_cfg4_small", 500, 4, None),
+                                                       ("tissue_cfg4_small", 500, 4, 1)])
+def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path, monkeypatch, name, steps, kind,
+                                           sweep_min):
     """The multi-rank GPU path (RCB boxes, rank-local problems: class-table
     stencil on the slab, diagonal operator on the ventricle; device-scalar
     pipelined PCG with the interior sweep overlapping the halo) with two
@@ -750,6 +758,8 @@ def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path, name, steps, kind):
 
     import torch.multiprocessing as mp
 
+    if sweep_min is not None:     # the workers inherit it: pcg_sweep_kernel with row classes
+        monkeypatch.setenv("MDX_SWEEP_MIN_ROWS", str(sweep_min))
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
