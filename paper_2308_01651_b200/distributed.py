@@ -112,6 +112,7 @@ class HaloComm:
         self.d_recv = torch.from_numpy(cat(self.recv_idx)).to(dev)
         self.nsend, self.nrecv = self.send_off[-1], self.recv_off[-1]
         self._bufs = {}
+        self._ops = {}
         self.bytes_per_vector = 8 * (self.nsend + self.nrecv)
 
     def _buffers(self, k, like):
@@ -162,19 +163,26 @@ class HaloComm:
         staged = dist.get_backend(self.group) == "gloo" and sbuf.is_cuda
         s_host = sbuf.cpu() if staged else sbuf
         r_host = rbuf.cpu() if staged else rbuf
-        ops = []
-        for i, q in enumerate(self.peers):
-            for j in range(k):
-                s0, s1 = self.send_off[i], self.send_off[i + 1]
-                r0, r1 = self.recv_off[i], self.recv_off[i + 1]
-                if s1 > s0:
-                    ops.append(dist.P2POp(dist.isend,
-                                          s_host[j * self.nsend + s0:j * self.nsend + s1], q,
-                                          group=self.group))
-                if r1 > r0:
-                    ops.append(dist.P2POp(dist.irecv,
-                                          r_host[j * self.nrecv + r0:j * self.nrecv + r1], q,
-                                          group=self.group))
+        # the pack buffers persist, so the op list of a (count, device) pair is built
+        # once (per CG iteration this is the host's largest cost on the exchange)
+        key = (k, sbuf.device.type)
+        ops = None if staged else self._ops.get(key)
+        if ops is None:
+            ops = []
+            for i, q in enumerate(self.peers):
+                for j in range(k):
+                    s0, s1 = self.send_off[i], self.send_off[i + 1]
+                    r0, r1 = self.recv_off[i], self.recv_off[i + 1]
+                    if s1 > s0:
+                        ops.append(dist.P2POp(dist.isend,
+                                              s_host[j * self.nsend + s0:j * self.nsend + s1],
+                                              q, group=self.group))
+                    if r1 > r0:
+                        ops.append(dist.P2POp(dist.irecv,
+                                              r_host[j * self.nrecv + r0:j * self.nrecv + r1],
+                                              q, group=self.group))
+            if not staged:
+                self._ops[key] = ops
         reqs = dist.batch_isend_irecv(ops) if ops else []
         return reqs, vectors, rbuf, r_host if staged else None
 
