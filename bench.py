@@ -18,8 +18,9 @@ untimed stepping from rest; W warm-up steps precede it.
 * ours: `value` is device-timed (CUDA events on the launch stream, barrier +
   synchronize both sides, max over ranks) with all state resident in HBM;
   `e2e` goes through the public API with host buffers: the window's start
-  state is uploaded from a checkpoint payload in pinned host memory
-  (TissueSolver.restore) inside the timed region, then the same K steps run
+  state is uploaded from a checkpoint payload in pinned host memory (the
+  reference's format with the history levels a restart of this BDF order
+  reads; TissueSolver.restore) inside the timed region, then the same K steps run
   and each writes its run() output row (u_min, u_max, 9 probes) into pinned
   host memory.  `secondary` is config 2 (442,401-node TTP06 slab) from step
   250 (t = 5 ms, mid-propagation).
@@ -399,7 +400,8 @@ def run_ours(args):
     solver.sync()
     window_from = solver.step_index
     # host copy of the window's start state (the e2e leg's input)
-    payload = solver.checkpoint_payload()
+    # (the history levels a BDF restart of this order reads; a valid reference payload)
+    payload = solver.checkpoint_payload(levels=cfg.bdf_order)
 
     # ---- device-timed region ------------------------------------------------
     with ClockSampler(local) as clocks:

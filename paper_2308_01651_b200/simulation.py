@@ -857,14 +857,20 @@ class TissueSolver:
 
     # -- checkpointing (simulation.py:518-631), reference byte format --------
 
-    def checkpoint_payload(self):
+    def checkpoint_payload(self, levels=None):
+        """The reference's MHEP body.  `levels` caps the history levels written
+        (None: every level the rings hold, like the reference; `bdf_order` levels
+        are all a restart needs - the format carries its own level counts, so the
+        reference's restore reads either)."""
         if self._pending:
             self.sync()
         n = self.n
+        cap = RING_SLOTS if levels is None else max(1, int(levels))
+        u_fill = min(self.u_fill, cap)
         parts = [struct.pack("<IQ", CHECKPOINT_VERSION, n),
                  struct.pack("<Qd", self.step_index, self.time),
-                 struct.pack("<I", self.u_fill)]
-        for k in range(self.u_fill):
+                 struct.pack("<I", u_fill)]
+        for k in range(u_fill):
             slot = (self.head - k) % RING_SLOTS
             parts.append(self.u_ring[slot, :n].cpu().numpy().tobytes())
         parts.append(self.act_time.cpu().numpy().tobytes())
@@ -875,7 +881,7 @@ class TissueSolver:
             label = vol.config.label.encode("utf-8")
             parts.append(struct.pack("<I", len(label)))
             parts.append(label)
-            fill = 1 if vol.config.disabled else vol.w_fill
+            fill = 1 if vol.config.disabled else min(vol.w_fill, cap)
             parts.append(struct.pack("<IQI", vol.num_vars, vol.dofs.size, fill))
             for k in range(fill):
                 slot = 0 if vol.config.disabled else (self.head - k) % RING_SLOTS

@@ -589,6 +589,17 @@ def test_checkpoint_format_and_cross_restore(golden, ns):
     s3 = TissueSolver(cfg)
     s3.restore(mine)
     assert s3.checkpoint_payload() == mine
+    # trimmed to the BDF order's history levels (bench.py's e2e input): shorter, and
+    # the continuation is bit-identical to the full payload's
+    short = s2.checkpoint_payload(levels=cfg.bdf_order)
+    assert len(short) < len(mine)
+    s4 = TissueSolver(cfg)
+    s4.restore(short)
+    assert s4.step_index == 400
+    s3.advance(50)
+    s4.advance(50)
+    assert np.array_equal(s3.potential, s4.potential)
+    assert np.array_equal(s3.iterations_log(), s4.iterations_log())
 
 
 def test_divergence_is_raised_and_state_rolls_back(ns):
