@@ -314,6 +314,90 @@ __global__ void __launch_bounds__(BLK, MINB) cg_iters(const Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = alpha + beta;
 }
 
+// Static sweeps with (ALT) consecutive sweeps running in opposite directions, so each
+// starts on the part of the vectors the previous one touched last, and (CS) the
+// operator's own-row coefficients loaded with the evict-first policy (ld.global.cs),
+// so the 658 MB operator stream does not push the 82 MB vectors out of the 126 MB L2.
+template <bool CS>
+__device__ __forceinline__ double dia_row_cs(const Dia& op, const double* __restrict__ vals,
+                                             const double* v, long i) {
+  const long ld = op.ld, last = op.n - 1;
+  double cl[NP], vl[NP], cu[NP], vu[NP];
+#pragma unroll
+  for (int s = 0; s < NP; ++s) {
+    const long d = op.off[s];
+    const double* cs = vals + (1 + s) * ld;
+    const long jl = i - d, jlc = jl < 0 ? 0 : jl, ju = i + d;
+    cl[s] = __ldg(cs + jlc);
+    vl[s] = v[jlc];
+    cu[s] = CS ? __ldcs(cs + i) : __ldg(cs + i);
+    vu[s] = v[ju > last ? last : ju];
+    if (jl < 0) cl[s] = 0.0;
+  }
+  const double dg = CS ? __ldcs(vals + i) : __ldg(vals + i), vc = v[i];
+  double acc = 0.0;
+#pragma unroll
+  for (int s = NP - 1; s >= 0; --s) acc = fma(cl[s], vl[s], acc);
+  acc = fma(dg, vc, acc);
+#pragma unroll
+  for (int s = 0; s < NP; ++s) acc = fma(cu[s], vu[s], acc);
+  return acc;
+}
+
+template <int NPT, bool ALT, bool CS>
+__global__ void __launch_bounds__(512, 2) cg_iters_alt(const Args a) {
+  __shared__ double sh[64];
+  const long n = a.op.n;
+  const long stride = (long)gridDim.x * blockDim.x;
+  const long tid0 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nbatch = (n + stride * NPT - 1) / (stride * NPT);
+  double alpha = 1e-9, beta = 0.5, rz = 1.0;
+  double* __restrict__ x = a.x;
+  double* r = a.r;
+  double* p = a.p;
+  double* q = a.q;
+  const double* __restrict__ dinv = a.dinv;
+  int sweep = 0;
+#define FOR_ROWS(...)                                                        \
+  for (long bb = 0; bb < nbatch; ++bb) {                                      \
+    const long b_ = (ALT && (sweep & 1)) ? nbatch - 1 - bb : bb;              \
+    _Pragma("unroll") for (int k = 0; k < NPT; ++k) {                         \
+      const long i = tid0 + (b_ * NPT + k) * stride;                          \
+      if (i < n) { __VA_ARGS__ }                                              \
+    }                                                                         \
+  }                                                                           \
+  ++sweep;
+  for (int it = 0; it < a.iters; ++it) {
+    FOR_ROWS({
+      const double zi = dinv[i] * r[i];
+      const double pi = p[i];
+      x[i] = fma(alpha, pi, x[i]);
+      p[i] = fma(beta, pi, zi);
+    })
+    grid_barrier(a.bar, gridDim.x);
+    double s1[1] = {0.0};
+    FOR_ROWS({
+      const double qi = dia_row_cs<CS>(a.op, a.vals, p, i);
+      q[i] = qi;
+      s1[0] = fma(p[i], qi, s1[0]);
+    })
+    grid_sum_blocks<1>(s1, a, sh);
+    alpha = 1e-9 + 1e-30 * s1[0];
+    double s2[2] = {0.0, 0.0};
+    FOR_ROWS({
+      const double ri = r[i] - alpha * q[i];
+      r[i] = ri;
+      const double zi = dinv[i] * ri;
+      s2[0] = fma(ri, ri, s2[0]);
+      s2[1] = fma(ri, zi, s2[1]);
+    })
+    grid_sum_blocks<2>(s2, a, sh);
+    beta = 0.5 + 1e-30 * (s2[1] / rz + s2[0]);
+  }
+#undef FOR_ROWS
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = alpha + beta;
+}
+
 // One kernel per sweep with the real reductions: every block leaves its partial,
 // the next kernel's blocks sum all partials (fixed order) to get alpha / beta.
 template <int NV>
@@ -499,6 +583,10 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     report("three kernels per iteration, CUDA graph", ms / a.iters * 1e3f);
   }
+  report("static  npt4 (alt kernel, no alt, no cs)", run(cg_iters_alt<4, false, false>, a, sms * 2, 512));
+  report("static  npt4 alternating directions", run(cg_iters_alt<4, true, false>, a, sms * 2, 512));
+  report("static  npt4 operator evict-first (ld.cs)", run(cg_iters_alt<4, false, true>, a, sms * 2, 512));
+  report("static  npt4 alternating + evict-first", run(cg_iters_alt<4, true, true>, a, sms * 2, 512));
   report("static  npt4 b512x2 +rem loads", run(cg_iters<0, 4, 512, 2, true>, a, sms * 2, 512));
   report("dyn Q   npt4 b512x2 (tile 2048)", run(cg_iters<1, 4, 512, 2, false>, a, sms * 2, 512));
   report("dyn QR  npt4 b512x2", run(cg_iters<2, 4, 512, 2, false>, a, sms * 2, 512));
