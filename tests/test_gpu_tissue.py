@@ -423,6 +423,63 @@ def test_cfg4_ventricle_100k_60ms(golden, ns):
     assert its.max() >= 20
 
 
+def test_cfg4_full_size_against_oracle_and_properties(ns):
+    """Config 4 at BASELINE's full size (10,276,240 nodes, 59.9 M tets, 3 volumes) - beyond
+    the reference itself (~28 h) - against the CPU oracle (pinned bit-for-bit
+    to the reference on the smaller meshes) over the first two steps from rest, plus
+    size-independent properties of the full-size operator and solve: the diagonal
+    storage with its 77,922-entry seam list is symmetric and positive, K has zero row
+    sums ((A_2 - A_1) 1 is a constant multiple of M 1), and the two- and three-sweep CG
+    forms agree step by step."""
+    import torch
+
+    from oracle import monodomain_oracle as O
+    from paper_2308_01651_b200 import ventricle
+    from paper_2308_01651_b200.simulation import TissueSolver
+
+    cfg = ventricle.config4(ns, *ventricle.size_for_nodes(1e7))
+    n = cfg.mesh.nodes.shape[0]
+    assert n == 10_276_240
+    s = TissueSolver(cfg)
+    assert s.op.kind == 4 and s.op.np_ == 7 and s.op.nrem == 77_922 and s.cg_variant == 1
+    # ---- the operator at full size --------------------------------------------------
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    y = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    A2 = s.op.a_tables[2]
+    Ax, Ay = _spmv(s.op, A2, x), _spmv(s.op, A2, y)
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    assert abs(yh @ Ax - xh @ Ay) <= 1e-11 * (np.abs(yh) @ np.abs(Ax))
+    assert xh @ Ax > 0 and yh @ Ay > 0
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    m1 = _spmv(s.op, s.op.d_m, one)
+    d = _spmv(s.op, A2, one) - _spmv(s.op, s.op.a_tables[1], one)
+    ratio = d / m1                       # (alpha_2 - alpha_1) chi C_m / dt on every row
+    assert m1.min() > 0
+    assert np.abs(ratio - np.median(ratio)).max() <= 1e-9 * abs(np.median(ratio))
+    # ---- two steps from rest against the oracle ---------------------------------------
+    orc = O.OracleTissue(cfg)
+    for _ in range(2):
+        s.enqueue_step()
+        orc.step()
+    s.sync()
+    its = s.iterations_log()
+    assert np.abs(its - np.array(orc.iters)).max() <= 1
+    assert its.max() >= 70               # the full-size solve's iteration counts (8 on 8,000 nodes)
+    assert _rel(s.potential, orc.potential) < 1e-8
+    del orc
+    # ---- the three-sweep form on the same steps ---------------------------------------
+    u1 = s.potential.copy()
+    del s
+    torch.cuda.empty_cache()
+    s0 = TissueSolver(cfg, cg_variant=0)
+    for _ in range(2):
+        s0.enqueue_step()
+    s0.sync()
+    assert np.abs(s0.iterations_log() - its).max() <= 1
+    assert _rel(s0.potential, u1) < 1e-9
+
+
 @pytest.mark.parametrize("key,steps", [("tissue_bo", 400), ("tissue_ttp", 1000)])
 def test_rush_larsen_tissue_vs_reference_functions(golden, ns, key, steps):
     """gate_scheme="rush_larsen": the reference TissueSolver at BDF1 with its ionic
