@@ -398,6 +398,150 @@ __global__ void __launch_bounds__(512, 2) cg_iters_alt(const Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = alpha + beta;
 }
 
+// Q sweep with the operator's own-row coefficients staged through shared memory by
+// TMA bulk copies (cp.async.bulk + mbarrier, STAGES tiles of 512 rows in flight per
+// block): the 64 B/row operator stream holds no registers while in flight, the
+// mirrored coefficient of a small offset comes from the staged tile.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(512, 2) cg_iters_tma(const Args a) {
+  constexpr int T = 512;
+  extern __shared__ __align__(128) double stage[];      // [STAGES][NP + 1][T]
+  __shared__ unsigned long long bars[STAGES];
+  __shared__ double sh[64];
+  const long n = a.op.n;
+  const long stride = (long)gridDim.x * blockDim.x;
+  const long tid0 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nb = (n + stride - 1) / stride;          // tiles per block
+  double alpha = 1e-9, beta = 0.5, rz = 1.0;
+  double* __restrict__ x = a.x;
+  double* r = a.r;
+  double* p = a.p;
+  double* q = a.q;
+  const double* __restrict__ dinv = a.dinv;
+  const double* vals = a.vals;
+  const long ld = a.op.ld, last = n - 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  long issued = 0, consumed = 0;     // tiles over the whole run (stage = count % STAGES)
+  auto issue = [&](long j) {         // thread 0: tile j of the current sweep
+    const long t0 = (j * gridDim.x + blockIdx.x) * (long)T;
+    if (t0 >= n) return;             // (empty tiles are not counted: parities stay aligned)
+    const unsigned rows = (unsigned)min((long)T, n - t0);
+    const int st = (int)(issued % STAGES);
+    mbar_expect_tx(&bars[st], (NP + 1) * rows * 8u);
+#pragma unroll
+    for (int c = 0; c <= NP; ++c)
+      tma_load_1d(stage + ((long)st * (NP + 1) + c) * T, vals + c * ld + t0, rows * 8u, &bars[st]);
+    ++issued;
+  };
+  for (int it = 0; it < a.iters; ++it) {
+    for (long base = tid0; base < n; base += stride * 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long i = base + k * stride;
+        if (i < n) {
+          const double zi = dinv[i] * r[i];
+          const double pi = p[i];
+          x[i] = fma(alpha, pi, x[i]);
+          p[i] = fma(beta, pi, zi);
+        }
+      }
+    }
+    // the operator tiles do not depend on p: start them before the barrier
+    if (threadIdx.x == 0)
+      for (long j = 0; j < STAGES - 1 && j < nb; ++j) issue(j);
+    grid_barrier(a.bar, gridDim.x);
+    double s1[1] = {0.0};
+    for (long j = 0; j < nb; ++j) {
+      if (threadIdx.x == 0 && j + STAGES - 1 < nb) issue(j + STAGES - 1);
+      const long i = tid0 + j * stride;
+      const int st = (int)(consumed % STAGES);
+      const unsigned parity = (unsigned)((consumed / STAGES) & 1);
+      if ((j * gridDim.x + blockIdx.x) * (long)T < n) {
+        mbar_wait(&bars[st], parity);
+        ++consumed;
+      }
+      if (i < n) {
+        const double* tile = stage + (long)st * (NP + 1) * T;
+        const int t = threadIdx.x;
+        double cl[NP], vl[NP], cu[NP], vu[NP];
+#pragma unroll
+        for (int s = 0; s < NP; ++s) {
+          const long d = a.op.off[s];
+          const long jl = i - d, jlc = jl < 0 ? 0 : jl, ju = i + d;
+          cl[s] = (d <= t) ? tile[(1 + s) * T + t - d] : __ldg(vals + (1 + s) * ld + jlc);
+          vl[s] = p[jlc];
+          cu[s] = tile[(1 + s) * T + t];
+          vu[s] = p[ju > last ? last : ju];
+          if (jl < 0) cl[s] = 0.0;
+        }
+        const double dg = tile[t], vc = p[i];
+        double acc = 0.0;
+#pragma unroll
+        for (int s = NP - 1; s >= 0; --s) acc = fma(cl[s], vl[s], acc);
+        acc = fma(dg, vc, acc);
+#pragma unroll
+        for (int s = 0; s < NP; ++s) acc = fma(cu[s], vu[s], acc);
+        q[i] = acc;
+        s1[0] = fma(vc, acc, s1[0]);
+      }
+      __syncthreads();    // the stage may be refilled
+    }
+    grid_sum_blocks<1>(s1, a, sh);
+    alpha = 1e-9 + 1e-30 * s1[0];
+    double s2[2] = {0.0, 0.0};
+    for (long base = tid0; base < n; base += stride * 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long i = base + k * stride;
+        if (i < n) {
+          const double ri = r[i] - alpha * q[i];
+          r[i] = ri;
+          const double zi = dinv[i] * ri;
+          s2[0] = fma(ri, ri, s2[0]);
+          s2[1] = fma(ri, zi, s2[1]);
+        }
+      }
+    }
+    grid_sum_blocks<2>(s2, a, sh);
+    beta = 0.5 + 1e-30 * (s2[1] / rz + s2[0]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = alpha + beta;
+}
+
 // One kernel per sweep with the real reductions: every block leaves its partial,
 // the next kernel's blocks sum all partials (fixed order) to get alpha / beta.
 template <int NV>
@@ -582,6 +726,36 @@ int main() {
     cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     report("three kernels per iteration, CUDA graph", ms / a.iters * 1e3f);
+  }
+  {
+    auto k3 = cg_iters_tma<3>;
+    const int smem3 = 3 * (NP + 1) * 512 * 8;
+    cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    void* params[] = {&a};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(a.bar, 0, 8);
+      cudaEventRecord(e0);
+      cudaLaunchCooperativeKernel((const void*)k3, dim3(sms * 2), dim3(512), params, smem3, 0);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+    }
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("  tma error: %s\n", cudaGetErrorString(e));
+    report("static  Q tiles staged by TMA (3 stages x 32 KB)", ms / a.iters * 1e3f);
+    auto k2 = cg_iters_tma<2>;
+    const int smem2 = 2 * (NP + 1) * 512 * 8;
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(a.bar, 0, 8);
+      cudaEventRecord(e0);
+      cudaLaunchCooperativeKernel((const void*)k2, dim3(sms * 2), dim3(512), params, smem2, 0);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) printf("  tma error: %s\n", cudaGetErrorString(e));
+    report("static  Q tiles staged by TMA (2 stages x 32 KB)", ms / a.iters * 1e3f);
   }
   report("static  npt4 (alt kernel, no alt, no cs)", run(cg_iters_alt<4, false, false>, a, sms * 2, 512));
   report("static  npt4 alternating directions", run(cg_iters_alt<4, true, false>, a, sms * 2, 512));
