@@ -787,7 +787,7 @@ def test_distributed_solver_single_rank_on_gpu(golden, monkeypatch, name, steps,
         dist.destroy_process_group()
 
 
-def _gloo_gpu_worker(rank, world, port, name, steps, out_dir):
+def _gloo_gpu_worker(rank, world, port, name, steps, out_dir, backend="gloo"):
     import os
     import sys
     from pathlib import Path
@@ -795,11 +795,17 @@ def _gloo_gpu_worker(rank, world, port, name, steps, out_dir):
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    import torch
     import torch.distributed as dist
 
     from paper_2308_01651_b200.distributed import DistributedTissueSolver
 
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":            # one GPU per rank
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", rank))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         s = DistributedTissueSolver(_dist_cfg(name))
         for _ in range(steps):
@@ -832,6 +838,36 @@ def test_distributed_two_ranks_on_gpu_gloo(golden, tmp_path, monkeypatch, name, 
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     mp.spawn(_gloo_gpu_worker, args=(2, port, name, steps, str(tmp_path)), nprocs=2,
+             join=True)
+    g = golden(name)
+    res = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
+    np.testing.assert_array_equal(res[0]["u"], res[1]["u"])
+    np.testing.assert_array_equal(res[0]["iters"], res[1]["iters"])
+    assert int(res[0]["kind"]) == kind
+    assert np.abs(res[0]["iters"] - g["iters"][:steps]).max() <= 1
+    assert _rel(res[0]["u"], g[f"snap_{steps}"]) < 1e-9
+
+
+@pytest.mark.parametrize("name,steps,kind", [("tissue_cfg0", 200, 1),
+                                             ("tissue_cfg4_small", 500, 4)])
+def test_distributed_two_ranks_nccl(golden, tmp_path, monkeypatch, name, steps, kind):
+    """Two ranks on two GPUs over NCCL: the packed halo exchange posted with
+    batch_isend_irecv on NCCL's stream while the interior rows are swept, the
+    boundary rows after work.wait(), one all-reduce per iteration - the stream
+    ordering the gloo tests cannot exercise.  Needs a box with two GPUs (skipped
+    on this pool's one-GPU boxes: NCCL refuses two ranks on one device)."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    monkeypatch.setenv("MDX_SWEEP_MIN_ROWS", "1")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.spawn(_gloo_gpu_worker, args=(2, port, name, steps, str(tmp_path), "nccl"), nprocs=2,
              join=True)
     g = golden(name)
     res = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
