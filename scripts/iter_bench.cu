@@ -659,21 +659,25 @@ float run(K kern, Args& a, int grid, int blk, int reps = 3) {
 int main() {
   const long n = 10276240;
   Args a;
-  a.op.n = n; a.op.ld = n;
+  const long ld_pad = getenv("IB_LD_PAD") ? atol(getenv("IB_LD_PAD")) : 0;       // doubles
+  const long stagger = getenv("IB_STAGGER") ? atol(getenv("IB_STAGGER")) : 0;     // doubles
+  const bool quick = getenv("IB_QUICK") != nullptr;
+  a.op.n = n; a.op.ld = n + ld_pad;
   const long nx = 41, nxy = 41 * 241;
   const long offs[NP] = {1, nx, nx + 1, nxy, nxy + 1, nxy + nx, nxy + nx + 1};
   for (int s = 0; s < NP; ++s) a.op.off[s] = offs[s];
   double *vals, *dinv;
   int* rem;
-  cudaMalloc(&vals, sizeof(double) * n * (NP + 1));
-  cudaMalloc(&a.r, sizeof(double) * n); cudaMalloc(&a.p, sizeof(double) * n);
-  cudaMalloc(&a.q, sizeof(double) * n); cudaMalloc(&a.x, sizeof(double) * n);
-  cudaMalloc(&dinv, sizeof(double) * n); cudaMalloc(&a.out, 64);
+  cudaMalloc(&vals, sizeof(double) * (n + ld_pad) * (NP + 1));
+  cudaMalloc(&a.r, sizeof(double) * (n + 8 * stagger)); cudaMalloc(&a.p, sizeof(double) * (n + 8 * stagger));
+  cudaMalloc(&a.q, sizeof(double) * (n + 8 * stagger)); cudaMalloc(&a.x, sizeof(double) * (n + 8 * stagger));
+  cudaMalloc(&dinv, sizeof(double) * (n + 8 * stagger)); cudaMalloc(&a.out, 64);
+  a.p += stagger; a.q += 2 * stagger; a.x += 3 * stagger; dinv += 4 * stagger;   // r stays
   cudaMalloc(&a.part, sizeof(double) * (4096 + 2 * 65536));
   cudaMalloc(&a.bar, 8); cudaMalloc(&a.ctr, 8);
   cudaMalloc(&rem, sizeof(int) * (n / 32 + 2)); cudaMemset(rem, 0, sizeof(int) * (n / 32 + 2));
   a.op.rem_ptr = rem; a.vals = vals; a.dinv = dinv;
-  fill<<<1024, 256>>>(vals, n * (NP + 1), 1e-3);
+  fill<<<1024, 256>>>(vals, (n + ld_pad) * (NP + 1), 1e-3);
   fill<<<1024, 256>>>(a.r, n, 1.0); fill<<<1024, 256>>>(a.p, n, 0.5); fill<<<1024, 256>>>(a.q, n, 0.25);
   fill<<<1024, 256>>>(a.x, n, 0.1); fill<<<1024, 256>>>(dinv, n, 2.0);
   cudaDeviceSynchronize();
@@ -688,6 +692,12 @@ int main() {
     Args b = a; b.iters = 200;
     float us = run(barriers_only<512, 2>, b, sms * 2, 512);
     printf("3 grid barriers alone (296 x 512): %.2f us per iteration\n", us);
+  }
+  if (quick) {
+    printf("ld_pad %ld stagger %ld\n", ld_pad, stagger);
+    for (int rep = 0; rep < 3; ++rep)
+      report("static  npt4 b512x2", run(cg_iters<0, 4, 512, 2, false>, a, sms * 2, 512));
+    return 0;
   }
   report("static  npt4 b512x2", run(cg_iters<0, 4, 512, 2, false>, a, sms * 2, 512));
   report("static  npt4 b512x2 barriers only (no sums)", run(cg_iters<0, 4, 512, 2, false, true>, a, sms * 2, 512));
